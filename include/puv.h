@@ -1,0 +1,181 @@
+/*
+ * puv.h — C ABI of libpuv: the differentiable splat render of UV-atlas Gaussians
+ * (PackUV-GS, arXiv 2602.23040) for NVIDIA B200 (sm_100a).
+ *
+ * The paper's problem statement: fit Gaussians stored in UV maps
+ * U[u,v,k] = {rho, r, s, o, c} to multi-view images by
+ * rendering them "as 2D splats ... combined with alpha-blending using a
+ * tile-based rasterizer" and back-propagating the image loss
+ * onto the texels, with gradient freezing of static Gaussians.
+ * Levels are packed into one atlas.  Every reading of a
+ * point the paper leaves open is listed in DESIGN.md §2 (R1..R16).
+ *
+ * Conventions (all entry points):
+ *  - extern "C", never throw; return puv_status (0 = PUV_OK, < 0 = error).
+ *  - The caller owns every buffer.  The library never allocates device memory.
+ *    "device pointer" = a pointer valid on the current CUDA device;
+ *    "host pointer" = ordinary process memory.  Arrays of device pointers
+ *    (plane tables) are themselves HOST arrays.
+ *  - Calls that take `stream` (a cudaStream_t, NULL = legacy default stream)
+ *    are asynchronous: argument errors are returned synchronously before any
+ *    work is enqueued; CUDA launch errors surface as PUV_E_CUDA.
+ *  - After an error, puv_last_error() returns a thread-local message.
+ *  - Texel planes are fp32, SoA: plane d of an atlas is H_A*W_A floats, row
+ *    major; texel id (gid) = y*W_A + x.  Plane order (R2):
+ *      [x, y, z, ls0, ls1, ls2, qw, qx, qy, qz, logit_o, sh(k,c) at 11+3k+c]
+ *    D = 11 + 3*(sh_degree+1)^2.
+ *  - Images are fp32 planar (3, H, W) per view, views concatenated.
+ */
+#ifndef PUV_H_
+#define PUV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t puv_status;
+enum {
+  PUV_OK = 0,
+  PUV_E_INVALID_ARGUMENT = -1,    /* null pointer, bad count, bad size */
+  PUV_E_INVALID_CONFIG = -2,      /* bad level list / sh_degree */
+  PUV_E_LAYOUT_OVERFLOW = -3,     /* placement outside the atlas */
+  PUV_E_DIMENSION_MISMATCH = -4,  /* plane count / image size mismatch */
+  PUV_E_INVALID_CAMERA = -5,      /* fx,fy <= 0, empty image, rotation not orthonormal within 1e-5 */
+  PUV_E_WORKSPACE_TOO_SMALL = -6, /* state buffer smaller than puv_query_sizes() */
+  PUV_E_STATE_MISMATCH = -7,      /* state was written by a different call signature */
+  PUV_E_CUDA = -8,                /* a CUDA runtime error (message in puv_last_error) */
+  PUV_E_UNSUPPORTED = -9          /* outside the built envelope (e.g. > 16 levels) */
+};
+
+#define PUV_MAX_LEVELS 16
+#define PUV_MAX_SH_DEGREE 3
+#define PUV_TILE 16
+
+/* One UV level placed in the atlas.  rows x cols = M_k x N_k.
+ * Unrotated: cell (r, c) -> atlas (y + r, x + c).  rot90ccw: the placement is
+ * cols tall and rows wide; cell (r, c) -> atlas (y + cols - 1 - c, x + r) (R15). */
+typedef struct {
+  int32_t rows, cols;
+  int32_t x, y;
+  int32_t rot90ccw;
+} puv_placement;
+
+typedef struct {
+  int32_t num_levels;   /* K, 1..16 */
+  int32_t sh_degree;    /* 0..3 */
+  int32_t planes;       /* D = 11 + 3*(sh_degree+1)^2 */
+  int32_t atlas_w, atlas_h;
+  puv_placement level[PUV_MAX_LEVELS];
+} puv_layout;
+
+/* Pinhole camera, OpenCV axes (x right, y down, z forward) (R4).  Pixel (i, j)
+ * is sampled at integer coordinates. */
+typedef struct {
+  float viewmat[16];    /* row-major world -> camera rigid transform */
+  float fx, fy, cx, cy; /* pixels */
+  int32_t width, height;
+  float near_plane;     /* cull z <= near (0.2 in every config) */
+  float campos[3];      /* camera centre in world space (SH view direction, R3) */
+} puv_camera;
+
+typedef struct {
+  float bg[3];          /* background colour, composited with T_final (R9) */
+  uint32_t flags;       /* reserved, must be 0 */
+} puv_render_opts;
+
+/* Column layout (R15): L0 at (0,0); levels 1.. stacked top-down at x = cols[0],
+ * unrotated; W_A = cols0 + max_{k>=1} cols_k, H_A = max(rows0, sum_{k>=1} rows_k).
+ * rows/cols: host arrays of K.  out: host. */
+puv_status puv_layout_for_levels(int32_t K, const int32_t* rows, const int32_t* cols, int32_t sh_degree,
+                                 puv_layout* out);
+
+/* Pack K levels into the atlas.  level_planes: host array of
+ * K*D device pointers, k-major (level k plane d at [k*D + d]), each rows_k*cols_k
+ * floats.  level_occ: host array of K device pointers to rows_k*cols_k bytes
+ * (occupancy), or NULL (all occupied).  atlas_planes: host array of D device
+ * pointers (H_A*W_A floats); atlas_occ: device, H_A*W_A bytes.  Pixels outside
+ * every placement are written 0 / unoccupied.  Errors: INVALID_ARGUMENT,
+ * LAYOUT_OVERFLOW (a placement leaves the atlas or two overlap). */
+puv_status puv_pack_atlas(const puv_layout* layout, const float* const* level_planes,
+                          const uint8_t* const* level_occ, float* const* atlas_planes, uint8_t* atlas_occ,
+                          void* stream);
+
+/* Inverse of pack for D planes (used for gradients): atlas -> levels. */
+puv_status puv_unpack_levels(const puv_layout* layout, const float* const* atlas_planes, float* const* level_planes,
+                             void* stream);
+
+/* Sizes for a render/backward call over n_views cameras (host array).
+ * state_bytes: the fixed-size per-call state (per-view records, depth order,
+ *   per-pixel transmittance, tile ranges, 2D gradients, scratch).
+ * arena_hint: a first guess for the key arena (tile lists); the exact need is
+ *   data dependent and reported by puv_check_overflow after a render. */
+puv_status puv_query_sizes(const puv_layout* layout, int32_t n_views, const puv_camera* cams,
+                           const puv_render_opts* opts, size_t* state_bytes, size_t* arena_hint);
+
+/* Forward render of n_views views (steps a1-a5 of DESIGN.md §1).
+ * atlas_planes: host array of D device pointers; atlas_occ: device H_A*W_A bytes
+ * or NULL (all occupied).  cams: host array of n_views.  images: device,
+ * n_views*3*H*W floats (all views must share W, H).  state: device, >= state_bytes.
+ * arena: device, arena_bytes (tile lists, 4 bytes per key).  If the keys do
+ * not fit, the overflow flag is set on device, the affected views render
+ * nothing, and puv_check_overflow reports the size needed. */
+puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                            int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, float* images,
+                            void* state, size_t state_bytes, void* arena, size_t arena_bytes, void* stream);
+
+/* L = 1/2 sum (images - targets)^2 (R11) over n floats; dL_dimages = images -
+ * targets.  loss: device double, OVERWRITTEN with L.  All device pointers. */
+puv_status puv_l2_loss_grad(int64_t n, const float* images, const float* targets, float* dL_dimages, double* loss,
+                            void* stream);
+
+/* Backward of the last puv_render_views with the same layout/cams/opts/state/arena
+ * (steps a7-a9).  dL_dimages: device, like images.  dynamic_mask: device
+ * H_A*W_A bytes (D_i of PAPER.md:410-414) or NULL.  atlas_grad: host array of D
+ * device pointers; gradients w.r.t. the texel planes are ACCUMULATED (+=). */
+puv_status puv_render_backward(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                               int32_t n_views, const puv_camera* cams, const puv_render_opts* opts,
+                               const float* dL_dimages, const uint8_t* dynamic_mask, void* state, size_t state_bytes,
+                               void* arena, size_t arena_bytes, float* const* atlas_grad, void* stream);
+
+/* The one host synchronisation per step: waits for `stream`, then reports
+ * whether any view of the last render overflowed the arena and the arena
+ * bytes the call needs.  Host outputs. */
+puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, int32_t* overflowed,
+                              uint64_t* needed_arena_bytes);
+
+/* Per-view debug/parity view of the state (synchronises `stream`).  Host out.
+ * Device pointers inside point into state/arena and stay valid until the next call. */
+typedef struct {
+  uint32_t n_visible;            /* Gaussians surviving culling in this view */
+  uint32_t ntiles, tiles_x, tiles_y;
+  uint64_t n_keys;               /* K = sum of tiles touched */
+  const uint32_t* tile_start;    /* device, ntiles: range start into `keys_gid` */
+  const uint32_t* tile_end;      /* device, ntiles: range end (exclusive) */
+  const uint32_t* keys_gid;      /* device, n_keys gids, sorted by (tile, depth_bits, gid) */
+  const uint32_t* depth_key;     /* device, H_A*W_A: depth bits of z, 0xFFFFFFFF if culled */
+  const float* t_final;          /* device, H*W: fp32 contract transmittance after the last entry */
+  const uint32_t* n_contrib;     /* device, H*W: list position after the last composited entry */
+  const double* grad2d;          /* device, H_A*W_A*9 fp64: per-Gaussian 2D grads (mx,my,ha,nb,hc,o,r,g,b) of the last backward */
+  const uint32_t* depth_order;   /* device, n_visible gids sorted by (depth_bits, gid) */
+} puv_view_debug;
+
+puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, const void* state,
+                          size_t state_bytes, const void* arena, int32_t view, void* stream, puv_view_debug* out);
+
+/* Evaluate a contract function of DESIGN.md R13 elementwise on device arrays (for the
+ * exhaustive GPU-vs-oracle bit-equality test).  op: 0 = exp_c, 1 = log_c.  in/out: device, n floats. */
+puv_status puv_debug_contract(int32_t op, const float* in, float* out, int64_t n, void* stream);
+
+/* Thread-local message of the last error; returns its length (writes up to len-1 chars + NUL). */
+size_t puv_last_error(char* buf, size_t len);
+
+/* Library build id, e.g. "libpuv sm_100a <git describe>". */
+const char* puv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PUV_H_ */

@@ -1,0 +1,385 @@
+// api.cu — the C ABI of include/puv.h: validation, state carving, stream sequencing.
+//
+// Host runtime only: every step of the path runs in the kernels of this
+// directory.  Argument errors are returned before anything is enqueued.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+#ifndef PUV_VERSION
+#define PUV_VERSION "dev"
+#endif
+
+namespace puv {
+
+static thread_local std::string g_err;
+
+static puv_status fail(puv_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+static puv_status cuda_check(const char* where) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PUV_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
+  return PUV_OK;
+}
+
+static puv_status check_layout(const puv_layout* L) {
+  if (!L) return fail(PUV_E_INVALID_ARGUMENT, "layout is NULL");
+  if (L->num_levels < 1 || L->num_levels > PUV_MAX_LEVELS)
+    return fail(PUV_E_INVALID_CONFIG, "num_levels %d outside 1..%d", L->num_levels, PUV_MAX_LEVELS);
+  if (L->sh_degree < 0 || L->sh_degree > PUV_MAX_SH_DEGREE)
+    return fail(PUV_E_INVALID_CONFIG, "sh_degree %d outside 0..3", L->sh_degree);
+  const int D = 11 + 3 * (L->sh_degree + 1) * (L->sh_degree + 1);
+  if (L->planes != D) return fail(PUV_E_DIMENSION_MISMATCH, "planes %d != 11 + 3 (deg+1)^2 = %d", L->planes, D);
+  if (L->atlas_w < 1 || L->atlas_h < 1 || (int64_t)L->atlas_w * L->atlas_h >= (int64_t)1 << 31)
+    return fail(PUV_E_INVALID_CONFIG, "atlas %d x %d", L->atlas_w, L->atlas_h);
+  for (int k = 0; k < L->num_levels; ++k) {
+    const puv_placement& a = L->level[k];
+    if (a.rows < 1 || a.cols < 1) return fail(PUV_E_INVALID_CONFIG, "level %d is empty", k);
+    const int w = a.rot90ccw ? a.rows : a.cols, h = a.rot90ccw ? a.cols : a.rows;
+    if (a.x < 0 || a.y < 0 || a.x + w > L->atlas_w || a.y + h > L->atlas_h)
+      return fail(PUV_E_LAYOUT_OVERFLOW, "level %d (%dx%d at %d,%d) leaves the %dx%d atlas", k, h, w, a.x, a.y,
+                  L->atlas_w, L->atlas_h);
+    for (int j = 0; j < k; ++j) {
+      const puv_placement& b = L->level[j];
+      const int wb = b.rot90ccw ? b.rows : b.cols, hb = b.rot90ccw ? b.cols : b.rows;
+      if (a.x < b.x + wb && b.x < a.x + w && a.y < b.y + hb && b.y < a.y + h)
+        return fail(PUV_E_LAYOUT_OVERFLOW, "levels %d and %d overlap", j, k);
+    }
+  }
+  return PUV_OK;
+}
+
+static puv_status check_cameras(int n, const puv_camera* cams, int& W, int& H) {
+  if (n < 1) return fail(PUV_E_INVALID_ARGUMENT, "n_views %d < 1", n);
+  if (!cams) return fail(PUV_E_INVALID_ARGUMENT, "cams is NULL");
+  W = cams[0].width;
+  H = cams[0].height;
+  for (int i = 0; i < n; ++i) {
+    const puv_camera& c = cams[i];
+    if (!(c.fx > 0.f) || !(c.fy > 0.f) || c.width < 1 || c.height < 1 || !(c.near_plane > 0.f))
+      return fail(PUV_E_INVALID_CAMERA, "camera %d: fx, fy, near must be > 0 and the image non-empty", i);
+    if (c.width != W || c.height != H)
+      return fail(PUV_E_DIMENSION_MISMATCH, "camera %d: %dx%d differs from camera 0 (%dx%d)", i, c.width, c.height, W, H);
+    if ((int64_t)W * H >= (int64_t)1 << 30 || (W + kTile - 1) / kTile > 65535 || (H + kTile - 1) / kTile > 65535)
+      return fail(PUV_E_UNSUPPORTED, "camera %d: image %dx%d too large", i, W, H);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double dot = 0;
+        for (int k = 0; k < 3; ++k) dot += (double)c.viewmat[4 * a + k] * c.viewmat[4 * b + k];
+        if (std::fabs(dot - (a == b ? 1.0 : 0.0)) > 1e-5)
+          return fail(PUV_E_INVALID_CAMERA, "camera %d: rotation not orthonormal within 1e-5", i);
+      }
+    if (c.viewmat[12] != 0.f || c.viewmat[13] != 0.f || c.viewmat[14] != 0.f || c.viewmat[15] != 1.f)
+      return fail(PUV_E_INVALID_CAMERA, "camera %d: last row of viewmat must be (0,0,0,1)", i);
+  }
+  return PUV_OK;
+}
+
+static CamDev cam_dev(const puv_camera& c) {
+  CamDev d;
+  for (int k = 0; k < 12; ++k) d.V[k] = c.viewmat[k];
+  d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
+  d.W = c.width; d.H = c.height;
+  d.near_plane = c.near_plane;
+  for (int k = 0; k < 3; ++k) d.campos[k] = c.campos[k];
+  // R5: lim = 1.3 * tan(fov/2) = 1.3 * 0.5 * W / fx in fp64, rounded to fp32
+  d.limx = (float)(1.3 * 0.5 * (double)c.width / (double)c.fx);
+  d.limy = (float)(1.3 * 0.5 * (double)c.height / (double)c.fy);
+  return d;
+}
+
+Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
+  Plan p{};
+  p.n_views = n_views;
+  p.N = L.atlas_w * L.atlas_h;
+  p.W = W; p.H = H; p.HW = W * H;
+  p.gx = (W + kTile - 1) / kTile;
+  p.gy = (H + kTile - 1) / kTile;
+  p.ntiles = p.gx * p.gy;
+  p.D = L.planes;
+  p.deg = L.sh_degree;
+  const size_t V = n_views, N = p.N;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off += align_up(bytes); return o; };
+  p.call_hdr = take(sizeof(CallHdr));
+  p.view_hdr = take(sizeof(ViewHdr) * V);
+  p.depth = take(4 * V * N);
+  p.rect = take(8 * V * N);
+  p.rec = take(48 * V * N);
+  p.rec64 = take(80 * V * N);
+  p.grad2d = take(72 * V * N);
+  p.sorted = take(4 * V * N);
+  p.tstart = take(4 * V * p.ntiles);
+  p.tend = take(4 * V * p.ntiles);
+  p.tfinal = take(4 * V * p.HW);
+  p.ncontrib = take(4 * V * p.HW);
+  p.sort_blocks = (N + 2047) / 2048;
+  p.sk0 = take(4 * N);
+  p.sv0 = take(4 * N);
+  p.sk1 = take(4 * N);
+  p.sv1 = take(4 * N);
+  p.hist = take(4 * 256 * p.sort_blocks);
+  p.koff = take(4 * (N + 1));
+  p.bsum = take(4 * (N / 2048 + 2));
+  p.cnt = take(4 * (size_t)kNbMax * p.ntiles);
+  p.total = off;
+  return p;
+}
+
+Views views_of(const Plan& p, void* state) {
+  char* s = (char*)state;
+  Views v;
+  v.depth = (uint32_t*)(s + p.depth);
+  v.rect = (uint2*)(s + p.rect);
+  v.rec = (float4*)(s + p.rec);
+  v.rec64 = (double2*)(s + p.rec64);
+  v.grad2d = (double*)(s + p.grad2d);
+  v.sorted = (uint32_t*)(s + p.sorted);
+  v.tstart = (uint32_t*)(s + p.tstart);
+  v.tend = (uint32_t*)(s + p.tend);
+  v.tfinal = (float*)(s + p.tfinal);
+  v.ncontrib = (uint32_t*)(s + p.ncontrib);
+  v.hdr = (ViewHdr*)(s + p.view_hdr);
+  v.call = (CallHdr*)(s + p.call_hdr);
+  return v;
+}
+
+struct Common {
+  Plan plan;
+  Views views;
+  PlaneTab P;
+  int W, H;
+};
+
+static puv_status prepare(const puv_layout* L, const float* const* atlas_planes, int32_t n_views,
+                          const puv_camera* cams, const puv_render_opts* opts, void* state, size_t state_bytes,
+                          Common& c) {
+  puv_status st = check_layout(L);
+  if (st) return st;
+  if (!atlas_planes) return fail(PUV_E_INVALID_ARGUMENT, "atlas_planes is NULL");
+  for (int d = 0; d < L->planes; ++d)
+    if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+  if (opts && opts->flags != 0) return fail(PUV_E_UNSUPPORTED, "opts.flags must be 0");
+  st = check_cameras(n_views, cams, c.W, c.H);
+  if (st) return st;
+  if (!state) return fail(PUV_E_INVALID_ARGUMENT, "state is NULL");
+  c.plan = make_plan(*L, n_views, c.W, c.H);
+  if (state_bytes < c.plan.total)
+    return fail(PUV_E_WORKSPACE_TOO_SMALL, "state_bytes %zu < %zu", state_bytes, c.plan.total);
+  c.views = views_of(c.plan, state);
+  for (int d = 0; d < L->planes; ++d) c.P.p[d] = atlas_planes[d];
+  return PUV_OK;
+}
+
+}  // namespace puv
+
+using namespace puv;
+
+extern "C" {
+
+puv_status puv_layout_for_levels(int32_t K, const int32_t* rows, const int32_t* cols, int32_t sh_degree,
+                                 puv_layout* out) {
+  if (!rows || !cols || !out) return fail(PUV_E_INVALID_ARGUMENT, "NULL argument");
+  if (K < 1 || K > PUV_MAX_LEVELS) return fail(PUV_E_INVALID_CONFIG, "K %d outside 1..%d", K, PUV_MAX_LEVELS);
+  if (sh_degree < 0 || sh_degree > PUV_MAX_SH_DEGREE) return fail(PUV_E_INVALID_CONFIG, "sh_degree %d", sh_degree);
+  puv_layout L;
+  std::memset(&L, 0, sizeof L);
+  L.num_levels = K;
+  L.sh_degree = sh_degree;
+  L.planes = 11 + 3 * (sh_degree + 1) * (sh_degree + 1);
+  int64_t y = 0, colw = 0;
+  for (int k = 0; k < K; ++k) {
+    if (rows[k] < 1 || cols[k] < 1) return fail(PUV_E_INVALID_CONFIG, "level %d is empty", k);
+    L.level[k].rows = rows[k];
+    L.level[k].cols = cols[k];
+    L.level[k].rot90ccw = 0;
+    if (k == 0) { L.level[k].x = 0; L.level[k].y = 0; continue; }
+    L.level[k].x = cols[0];
+    L.level[k].y = (int32_t)y;
+    y += rows[k];
+    if (cols[k] > colw) colw = cols[k];
+  }
+  const int64_t W = (int64_t)cols[0] + colw, H = rows[0] > y ? rows[0] : y;
+  if (W * H >= (int64_t)1 << 31) return fail(PUV_E_LAYOUT_OVERFLOW, "atlas %lld x %lld too large", (long long)W,
+                                               (long long)H);
+  L.atlas_w = (int32_t)W;
+  L.atlas_h = (int32_t)H;
+  *out = L;
+  return PUV_OK;
+}
+
+puv_status puv_pack_atlas(const puv_layout* layout, const float* const* level_planes, const uint8_t* const* level_occ,
+                          float* const* atlas_planes, uint8_t* atlas_occ, void* stream) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  if (!level_planes || !atlas_planes || !atlas_occ) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer table");
+  for (int i = 0; i < layout->num_levels * layout->planes; ++i)
+    if (!level_planes[i]) return fail(PUV_E_INVALID_ARGUMENT, "level plane %d is NULL", i);
+  for (int d = 0; d < layout->planes; ++d)
+    if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+  launch_pack(*layout, level_planes, level_occ, atlas_planes, atlas_occ, (cudaStream_t)stream);
+  return cuda_check("puv_pack_atlas");
+}
+
+puv_status puv_unpack_levels(const puv_layout* layout, const float* const* atlas_planes, float* const* level_planes,
+                             void* stream) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  if (!level_planes || !atlas_planes) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer table");
+  launch_unpack(*layout, atlas_planes, level_planes, (cudaStream_t)stream);
+  return cuda_check("puv_unpack_levels");
+}
+
+puv_status puv_query_sizes(const puv_layout* layout, int32_t n_views, const puv_camera* cams,
+                           const puv_render_opts* opts, size_t* state_bytes, size_t* arena_hint) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  int W, H;
+  st = check_cameras(n_views, cams, W, H);
+  if (st) return st;
+  if (!state_bytes || !arena_hint) return fail(PUV_E_INVALID_ARGUMENT, "NULL output");
+  const Plan p = make_plan(*layout, n_views, W, H);
+  *state_bytes = p.total;
+  // first guess: 48 keys per Gaussian per view (C3 measures ~37-43)
+  *arena_hint = (size_t)4 * 48 * (size_t)p.N * n_views;
+  return PUV_OK;
+}
+
+puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                            int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, float* images,
+                            void* state, size_t state_bytes, void* arena, size_t arena_bytes, void* stream) {
+  Common c;
+  puv_status st = prepare(layout, atlas_planes, n_views, cams, opts, state, state_bytes, c);
+  if (st) return st;
+  if (!images) return fail(PUV_E_INVALID_ARGUMENT, "images is NULL");
+  if (!arena && arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "arena is NULL");
+  const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
+  cudaStream_t s = (cudaStream_t)stream;
+  const Plan& p = c.plan;
+  launch_begin_call(p, c.views, arena_bytes / 4, s);
+  for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
+    CamBatch cb;
+    cb.v0 = v0;
+    cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
+    for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
+    launch_project(p, c.views, c.P, atlas_occ, cb, s);
+  }
+  for (int v = 0; v < n_views; ++v) {
+    launch_depth_sort(p, c.views, state, v, s);
+    launch_bin(p, c.views, state, (uint32_t*)arena, v, s);
+    launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)v * 3 * p.HW, v, bg, s);
+  }
+  return cuda_check("puv_render_views");
+}
+
+puv_status puv_l2_loss_grad(int64_t n, const float* images, const float* targets, float* dL_dimages, double* loss,
+                            void* stream) {
+  if (n < 0 || (n > 0 && (!images || !targets || !dL_dimages)) || !loss)
+    return fail(PUV_E_INVALID_ARGUMENT, "bad loss arguments");
+  launch_l2_loss(n, images, targets, dL_dimages, loss, (cudaStream_t)stream);
+  return cuda_check("puv_l2_loss_grad");
+}
+
+puv_status puv_render_backward(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                               int32_t n_views, const puv_camera* cams, const puv_render_opts* opts,
+                               const float* dL_dimages, const uint8_t* dynamic_mask, void* state, size_t state_bytes,
+                               void* arena, size_t arena_bytes, float* const* atlas_grad, void* stream) {
+  Common c;
+  puv_status st = prepare(layout, atlas_planes, n_views, cams, opts, state, state_bytes, c);
+  if (st) return st;
+  if (!dL_dimages || !atlas_grad) return fail(PUV_E_INVALID_ARGUMENT, "NULL dL_dimages / atlas_grad");
+  GradTab G;
+  for (int d = 0; d < layout->planes; ++d) {
+    if (!atlas_grad[d]) return fail(PUV_E_INVALID_ARGUMENT, "grad plane %d is NULL", d);
+    G.p[d] = atlas_grad[d];
+  }
+  const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
+  cudaStream_t s = (cudaStream_t)stream;
+  const Plan& p = c.plan;
+  for (int v = 0; v < n_views; ++v)
+    launch_raster_bwd(p, c.views, (const uint32_t*)arena, dL_dimages + (size_t)v * 3 * p.HW, v, bg, s);
+  for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
+    CamBatch cb;
+    cb.v0 = v0;
+    cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
+    for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
+    launch_project_bwd(p, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s);
+  }
+  return cuda_check("puv_render_backward");
+}
+
+puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, int32_t* overflowed,
+                              uint64_t* needed_arena_bytes) {
+  if (!state || !overflowed || !needed_arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "NULL argument");
+  CallHdr h;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemcpyAsync(&h, state, sizeof h, cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(PUV_E_CUDA, "puv_check_overflow: %s", cudaGetErrorString(e));
+  *overflowed = (int32_t)h.overflow_any;
+  *needed_arena_bytes = 4 * h.arena_need;
+  return PUV_OK;
+}
+
+puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, const void* state,
+                          size_t state_bytes, const void* arena, int32_t view, void* stream, puv_view_debug* out) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  int W, H;
+  st = check_cameras(n_views, cams, W, H);
+  if (st) return st;
+  if (!state || !out || view < 0 || view >= n_views) return fail(PUV_E_INVALID_ARGUMENT, "bad debug arguments");
+  const Plan p = make_plan(*layout, n_views, W, H);
+  if (state_bytes < p.total) return fail(PUV_E_WORKSPACE_TOO_SMALL, "state too small");
+  const Views v = views_of(p, (void*)state);
+  ViewHdr h;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemcpyAsync(&h, v.hdr + view, sizeof h, cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(PUV_E_CUDA, "puv_debug_view: %s", cudaGetErrorString(e));
+  out->n_visible = h.n_vis;
+  out->ntiles = p.ntiles;
+  out->tiles_x = p.gx;
+  out->tiles_y = p.gy;
+  out->n_keys = h.overflow ? 0 : h.K;
+  out->tile_start = v.tstart + (size_t)view * p.ntiles;
+  out->tile_end = v.tend + (size_t)view * p.ntiles;
+  out->keys_gid = (const uint32_t*)arena + h.list_base;
+  out->depth_key = v.depth + (size_t)view * p.N;
+  out->t_final = v.tfinal + (size_t)view * p.HW;
+  out->n_contrib = v.ncontrib + (size_t)view * p.HW;
+  out->grad2d = v.grad2d + (size_t)view * p.N * 9;
+  out->depth_order = v.sorted + (size_t)view * p.N;
+  return PUV_OK;
+}
+
+puv_status puv_debug_contract(int32_t op, const float* in, float* out, int64_t n, void* stream) {
+  if ((op != 0 && op != 1) || n < 0 || (n > 0 && (!in || !out))) return fail(PUV_E_INVALID_ARGUMENT, "bad contract args");
+  if (n) launch_contract(op, in, out, n, (cudaStream_t)stream);
+  return cuda_check("puv_debug_contract");
+}
+
+size_t puv_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    const size_t n = g_err.size() < len - 1 ? g_err.size() : len - 1;
+    std::memcpy(buf, g_err.data(), n);
+    buf[n] = 0;
+  }
+  return g_err.size();
+}
+
+const char* puv_version(void) { return "libpuv sm_100a " PUV_VERSION; }
+
+}  // extern "C"

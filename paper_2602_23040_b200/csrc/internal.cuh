@@ -1,0 +1,103 @@
+// internal.cuh — device-side types, state layout and launchers of libpuv.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/puv.h"
+
+namespace puv {
+
+constexpr int kMaxPlanes = 11 + 3 * 16;   // SH degree 3
+constexpr int kCamBatch = 64;             // views per K1/K7 launch (cameras passed by value, 6 KB of params)
+constexpr int kTile = PUV_TILE;
+constexpr int kNbMax = 1024;              // max key blocks of the stable tile pass per view
+constexpr uint32_t kInvisible = 0xFFFFFFFFu;
+
+struct PlaneTab { const float* p[kMaxPlanes]; };
+struct GradTab { float* p[kMaxPlanes]; };
+
+// Per-view camera constants (viewmat rows 0..2, intrinsics, lim = fp32(1.3*W/(2 fx)) (R5)).
+struct CamDev {
+  float V[12];
+  float fx, fy, cx, cy;
+  int W, H;
+  float near_plane;
+  float campos[3];
+  float limx, limy;
+};
+struct CamBatch { CamDev c[kCamBatch]; int n; int v0; };
+
+// Device header of one view (written by kernels; read by later kernels and by the host once per step).
+struct ViewHdr {
+  uint32_t n_vis;
+  uint32_t overflow;      // 1 if this view's keys did not fit in the arena
+  uint64_t K;             // keys of this view
+  uint64_t list_base;     // offset (in keys) of this view's lists inside the arena
+  uint32_t kb;            // keys per block of the stable tile pass
+  uint32_t nb;            // blocks of the stable tile pass
+  uint64_t pad[4];
+};
+struct CallHdr {
+  uint64_t arena_used;    // keys handed out so far (running sum over views)
+  uint64_t arena_need;    // keys requested (>= arena_used when overflowing)
+  uint32_t overflow_any;
+  uint32_t pad0;
+  uint64_t arena_cap;     // capacity in keys (copied at launch)
+  uint64_t pad[4];
+};
+
+// Offsets (bytes) of every array inside the caller's state buffer.
+struct Plan {
+  int n_views, N, W, H, HW, gx, gy, ntiles, D, deg;
+  size_t call_hdr, view_hdr;
+  // per view arrays, each [n_views][...]
+  size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib;
+  // scratch shared by all views (reused in stream order)
+  size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt;
+  size_t sort_blocks;      // blocks of one radix pass over N items
+  size_t total;
+};
+
+// Records of a visible (view, Gaussian):
+//  rec   (fp32 contract, 48 B): A=(mx,my,ha,nb) B=(hc,t_g,o,-) C=(r,g,b,flags)   -> decisions + forward image
+//  rec64 (fp64 values,   80 B): (mx,my) (ha,nb) (hc,o) (r,g) (b,-)               -> backward values
+struct Views {
+  uint32_t* depth;   // [V][N]
+  uint2* rect;       // [V][N]  (x0 | x1<<16, y0 | y1<<16)
+  float4* rec;       // [V][N][3]
+  double2* rec64;    // [V][N][5]
+  double* grad2d;    // [V][N][9]  d/d(mx,my,ha,nb,hc,o,r,g,b), fp64
+  uint32_t* sorted;  // [V][N]  gids in (depth, gid) order, first n_vis valid
+  uint32_t* tstart;  // [V][ntiles]
+  uint32_t* tend;    // [V][ntiles]
+  float* tfinal;     // [V][HW]
+  uint32_t* ncontrib;// [V][HW]
+  ViewHdr* hdr;      // [V]
+  CallHdr* call;
+};
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+Plan make_plan(const puv_layout& L, int n_views, int W, int H);
+Views views_of(const Plan& p, void* state);
+
+// ---- launchers (all asynchronous on `s`) ----
+void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,
+                    cudaStream_t s);
+void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cudaStream_t s);
+void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
+void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* image, int view,
+                       const float bg[3], cudaStream_t s);
+void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimage, int view,
+                       const float bg[3], cudaStream_t s);
+void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const uint8_t* mask,
+                        const CamBatch& cb, const GradTab& G, cudaStream_t s);
+void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s);
+void launch_pack(const puv_layout& L, const float* const* level_planes, const uint8_t* const* level_occ,
+                 float* const* atlas_planes, uint8_t* atlas_occ, cudaStream_t s);
+void launch_unpack(const puv_layout& L, const float* const* atlas_planes, float* const* level_planes, cudaStream_t s);
+void launch_contract(int op, const float* in, float* out, int64_t n, cudaStream_t s);
+void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaStream_t s);
+
+}  // namespace puv

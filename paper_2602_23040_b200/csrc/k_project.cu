@@ -1,0 +1,99 @@
+// K1 k_project — fused atlas unpack + EWA projection + SH colour + tile rect (rows a1, a2).
+//
+// One thread per texel; the texel's planes are read ONCE (coalesced SoA loads)
+// and the thread loops over up to kCamBatch views.  Per visible (view, Gaussian)
+// it writes: the depth key and tile rect (fp32 contract, R13 -> binning), the
+// 48-byte fp32 record (contract conic/mean/t_g/o + colour -> forward raster and
+// every compositing decision) and the 80-byte fp64 value record (the same
+// quantities in double -> backward).  It also zeroes the
+// (view, Gaussian) 2D-gradient slot that K6 accumulates into.
+#include "project.cuh"
+
+namespace puv {
+
+template <int DEG>
+__global__ void __launch_bounds__(128) k_project(PlaneTab P, const uint8_t* __restrict__ occ, int N,
+                                                 const __grid_constant__ CamBatch cb, Views v, int gx, int gy) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= N) return;
+  constexpr int NK = (DEG + 1) * (DEG + 1);
+  const bool occupied = occ == nullptr || occ[g] != 0;
+  const float mux = __ldg(P.p[0] + g), muy = __ldg(P.p[1] + g), muz = __ldg(P.p[2] + g);
+  const float ls0 = __ldg(P.p[3] + g), ls1 = __ldg(P.p[4] + g), ls2 = __ldg(P.p[5] + g);
+  const float qw = __ldg(P.p[6] + g), qx = __ldg(P.p[7] + g), qy = __ldg(P.p[8] + g), qz = __ldg(P.p[9] + g);
+  const float logit = __ldg(P.p[10] + g);
+  const Unpacked u = unpack_contract(ls0, ls1, ls2, qw, qx, qy, qz, logit);
+  bool any = false;
+  Unpacked64 u64;
+  float sh[3 * NK];
+
+  for (int i = 0; i < cb.n; ++i) {
+    const CamDev& c = cb.c[i];
+    const size_t o = (size_t)(cb.v0 + i) * (size_t)N + (size_t)g;
+    Proj pr;
+    pr.vis = false;
+    CamPoint cp;
+    if (occupied && u.ok) {
+      cp = cam_point(c, mux, muy, muz);
+      pr = project_contract(c, cp, u, gx, gy);
+    }
+    if (!pr.vis) {
+      v.depth[o] = kInvisible;
+      continue;
+    }
+    if (!any) {  // first visible view of this texel: fp64 unpack + SH coefficients
+      any = true;
+      u64 = unpack64(ls0, ls1, ls2, qw, qx, qy, qz, logit);
+#pragma unroll
+      for (int k = 0; k < 3 * NK; ++k) sh[k] = __ldg(P.p[11 + k] + g);
+    }
+    const Proj64 p64 = project64(c, mux, muy, muz, u64, cp.clx, cp.cly);
+    // SH colour (R3) in fp64; the clamp decision is recorded for K7
+    double dx = (double)mux - c.campos[0], dy = (double)muy - c.campos[1], dz = (double)muz - c.campos[2];
+    const double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+    dx *= inv; dy *= inv; dz *= inv;
+    double Y[NK];
+    sh_basis<DEG, double>(dx, dy, dz, Y);
+    double rgb[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      double acc = 0.5;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) acc = fma(Y[k], (double)sh[3 * k + ch], acc);
+      rgb[ch] = acc;
+    }
+    uint32_t flags = 0;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      if (rgb[ch] < 0.0) { rgb[ch] = 0.0; flags |= 1u << ch; }
+    v.depth[o] = pr.depth_bits;
+    v.rect[o] = make_uint2((uint32_t)pr.x0 | ((uint32_t)pr.x1 << 16), (uint32_t)pr.y0 | ((uint32_t)pr.y1 << 16));
+    float4* rec = v.rec + 3 * o;
+    rec[0] = make_float4(pr.mx, pr.my, pr.ha, pr.nb);
+    rec[1] = make_float4(pr.hc, u.t_g, u.o, 0.0f);
+    rec[2] = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], __uint_as_float(flags));
+    double2* r64 = v.rec64 + 5 * o;
+    r64[0] = make_double2(p64.mx, p64.my);
+    r64[1] = make_double2(p64.ha, p64.nb);
+    r64[2] = make_double2(p64.hc, u64.o);
+    r64[3] = make_double2(rgb[0], rgb[1]);
+    r64[4] = make_double2(rgb[2], 0.0);
+    double* g2 = v.grad2d + 9 * o;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) g2[k] = 0.0;
+  }
+}
+
+void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,
+                    cudaStream_t s) {
+  const int threads = 128;
+  const int blocks = (p.N + threads - 1) / threads;
+  switch (p.deg) {
+    case 0: k_project<0><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
+    case 1: k_project<1><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
+    case 2: k_project<2><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
+    default: k_project<3><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
+  }
+}
+
+}  // namespace puv

@@ -1,0 +1,292 @@
+"""Thin ctypes binding of libpuv (include/puv.h).  Argument marshalling only.
+
+Every step of the render runs in the CUDA kernels of `csrc/`; this module
+turns torch tensors into raw device pointers and the current CUDA stream into
+a `cudaStream_t`.  There is no CPU fallback: if `libpuv.so` is missing the
+import fails loudly (`RuntimeError`).
+
+Functions keep the C names without the `puv_` prefix: layout_for_levels,
+pack_atlas, unpack_levels, query_sizes, render_views, l2_loss_grad,
+render_backward, check_overflow, debug_view, last_error.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpuv.so")
+MAX_LEVELS = 16
+
+_status = {0: "PUV_OK", -1: "PUV_E_INVALID_ARGUMENT", -2: "PUV_E_INVALID_CONFIG", -3: "PUV_E_LAYOUT_OVERFLOW",
+           -4: "PUV_E_DIMENSION_MISMATCH", -5: "PUV_E_INVALID_CAMERA", -6: "PUV_E_WORKSPACE_TOO_SMALL",
+           -7: "PUV_E_STATE_MISMATCH", -8: "PUV_E_CUDA", -9: "PUV_E_UNSUPPORTED"}
+
+
+class PuvError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_status.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Placement(C.Structure):
+    _fields_ = [("rows", C.c_int32), ("cols", C.c_int32), ("x", C.c_int32), ("y", C.c_int32),
+                ("rot90ccw", C.c_int32)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("num_levels", C.c_int32), ("sh_degree", C.c_int32), ("planes", C.c_int32),
+                ("atlas_w", C.c_int32), ("atlas_h", C.c_int32), ("level", Placement * MAX_LEVELS)]
+
+
+class Camera(C.Structure):
+    _fields_ = [("viewmat", C.c_float * 16), ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float),
+                ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32), ("near_plane", C.c_float),
+                ("campos", C.c_float * 3)]
+
+
+class RenderOpts(C.Structure):
+    _fields_ = [("bg", C.c_float * 3), ("flags", C.c_uint32)]
+
+
+class ViewDebug(C.Structure):
+    _fields_ = [("n_visible", C.c_uint32), ("ntiles", C.c_uint32), ("tiles_x", C.c_uint32),
+                ("tiles_y", C.c_uint32), ("n_keys", C.c_uint64), ("tile_start", C.c_void_p),
+                ("tile_end", C.c_void_p), ("keys_gid", C.c_void_p), ("depth_key", C.c_void_p),
+                ("t_final", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
+                ("depth_order", C.c_void_p)]
+
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libpuv.so not built at {LIB_PATH}: run __graft_entry__.build() "
+                               "(make -C paper_2602_23040_b200/csrc); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        P, S = C.c_void_p, C.c_int32
+        L.puv_layout_for_levels.argtypes = [S, P, P, S, P]
+        L.puv_pack_atlas.argtypes = [P, P, P, P, P, P]
+        L.puv_unpack_levels.argtypes = [P, P, P, P]
+        L.puv_query_sizes.argtypes = [P, S, P, P, P, P]
+        L.puv_render_views.argtypes = [P, P, P, S, P, P, P, P, C.c_size_t, P, C.c_size_t, P]
+        L.puv_l2_loss_grad.argtypes = [C.c_int64, P, P, P, P, P]
+        L.puv_render_backward.argtypes = [P, P, P, S, P, P, P, P, P, C.c_size_t, P, C.c_size_t, P, P]
+        L.puv_check_overflow.argtypes = [P, S, P, P, P]
+        L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
+        L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
+        L.puv_last_error.argtypes = [C.c_char_p, C.c_size_t]
+        L.puv_last_error.restype = C.c_size_t
+        L.puv_version.restype = C.c_char_p
+        for f in ("puv_layout_for_levels", "puv_pack_atlas", "puv_unpack_levels", "puv_query_sizes",
+                  "puv_render_views", "puv_l2_loss_grad", "puv_render_backward", "puv_check_overflow",
+                  "puv_debug_view", "puv_debug_contract"):
+            getattr(L, f).restype = C.c_int32
+        _LIB = L
+    return _LIB
+
+
+def last_error() -> str:
+    buf = C.create_string_buffer(1024)
+    lib().puv_last_error(buf, 1024)
+    return buf.value.decode()
+
+
+def _ok(rc):
+    if rc != 0:
+        raise PuvError(rc, last_error())
+
+
+def version() -> str:
+    return lib().puv_version().decode()
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _ptr_table(tensors):
+    return (C.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+
+
+def _planes(t: torch.Tensor):
+    """(D, H, W) fp32 CUDA tensor -> host table of D plane pointers."""
+    assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous(), "planes: contiguous fp32 CUDA (D,H,W)"
+    return _ptr_table([t[d] for d in range(t.shape[0])])
+
+
+def camera(viewmat, fx, fy, cx, cy, width, height, near, campos) -> Camera:
+    c = Camera()
+    c.viewmat[:] = [float(x) for x in torch.as_tensor(viewmat, dtype=torch.float32).reshape(-1).tolist()]
+    c.fx, c.fy, c.cx, c.cy = float(fx), float(fy), float(cx), float(cy)
+    c.width, c.height, c.near_plane = int(width), int(height), float(near)
+    c.campos[:] = [float(x) for x in torch.as_tensor(campos, dtype=torch.float32).reshape(-1).tolist()]
+    return c
+
+
+def cameras(cams) -> C.Array:
+    """Sequence of objects with viewmat/fx/fy/cx/cy/width/height/near/campos (e.g. synth.scenes.Camera)."""
+    arr = (Camera * len(cams))()
+    for i, c in enumerate(cams):
+        arr[i] = camera(c.viewmat, c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.near, c.campos)
+    return arr
+
+
+def opts(bg=(0.0, 0.0, 0.0)) -> RenderOpts:
+    o = RenderOpts()
+    o.bg[:] = [float(x) for x in bg]
+    o.flags = 0
+    return o
+
+
+# ---------------------------------------------------------------------------------------------
+# entry points (same names as the C ABI)
+
+def layout_for_levels(shapes, sh_degree: int) -> Layout:
+    K = len(shapes)
+    rows = (C.c_int32 * K)(*[int(s[0]) for s in shapes])
+    cols = (C.c_int32 * K)(*[int(s[1]) for s in shapes])
+    out = Layout()
+    _ok(lib().puv_layout_for_levels(K, rows, cols, sh_degree, C.byref(out)))
+    return out
+
+
+def pack_atlas(layout: Layout, level_planes, level_occ=None, stream=None):
+    """level_planes: list of K (D, rows, cols) fp32 CUDA tensors; level_occ: list of K uint8 or None.
+    Returns (atlas (D, H_A, W_A) fp32, occ (H_A, W_A) uint8)."""
+    D = layout.planes
+    dev = level_planes[0].device
+    atlas = torch.empty((D, layout.atlas_h, layout.atlas_w), dtype=torch.float32, device=dev)
+    occ = torch.empty((layout.atlas_h, layout.atlas_w), dtype=torch.uint8, device=dev)
+    lp = _ptr_table([lv[d] for lv in level_planes for d in range(D)])
+    lo = _ptr_table(level_occ) if level_occ is not None else None
+    _ok(lib().puv_pack_atlas(C.byref(layout), lp, lo, _planes(atlas), _ptr(occ), _stream(stream)))
+    return atlas, occ
+
+
+def unpack_levels(layout: Layout, atlas: torch.Tensor, stream=None):
+    D = layout.planes
+    out = [torch.empty((D, layout.level[k].rows, layout.level[k].cols), dtype=torch.float32, device=atlas.device)
+           for k in range(layout.num_levels)]
+    lp = _ptr_table([lv[d] for lv in out for d in range(D)])
+    _ok(lib().puv_unpack_levels(C.byref(layout), _planes(atlas), lp, _stream(stream)))
+    return out
+
+
+def query_sizes(layout: Layout, cams, opts_=None):
+    sb, ah = C.c_size_t(), C.c_size_t()
+    _ok(lib().puv_query_sizes(C.byref(layout), len(cams), cams, C.byref(opts_) if opts_ else None,
+                              C.byref(sb), C.byref(ah)))
+    return sb.value, ah.value
+
+
+def render_views(layout, atlas, occ, cams, opts_, images, state, arena, stream=None):
+    _ok(lib().puv_render_views(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
+                               C.byref(opts_) if opts_ else None, _ptr(images), _ptr(state), state.numel(),
+                               _ptr(arena), arena.numel(), _stream(stream)))
+
+
+def l2_loss_grad(images, targets, dL, loss, stream=None):
+    _ok(lib().puv_l2_loss_grad(images.numel(), _ptr(images), _ptr(targets), _ptr(dL), _ptr(loss), _stream(stream)))
+
+
+def render_backward(layout, atlas, occ, cams, opts_, dL, mask, state, arena, grad, stream=None):
+    _ok(lib().puv_render_backward(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
+                                  C.byref(opts_) if opts_ else None, _ptr(dL), _ptr(mask), _ptr(state),
+                                  state.numel(), _ptr(arena), arena.numel(), _planes(grad), _stream(stream)))
+
+
+def check_overflow(state, n_views, stream=None):
+    ov, need = C.c_int32(), C.c_uint64()
+    _ok(lib().puv_check_overflow(_ptr(state), n_views, _stream(stream), C.byref(ov), C.byref(need)))
+    return bool(ov.value), int(need.value)
+
+
+def debug_view(layout, cams, state, arena, view, stream=None) -> ViewDebug:
+    out = ViewDebug()
+    _ok(lib().puv_debug_view(C.byref(layout), len(cams), cams, _ptr(state), state.numel(), _ptr(arena), view,
+                             _stream(stream), C.byref(out)))
+    return out
+
+
+def debug_contract(op: str, x: torch.Tensor, stream=None) -> torch.Tensor:
+    """exp_c / log_c of DESIGN.md R13 on a CUDA fp32 tensor (bit-equality tests)."""
+    out = torch.empty_like(x)
+    _ok(lib().puv_debug_contract({"exp_c": 0, "log_c": 1}[op], _ptr(x), _ptr(out), x.numel(), _stream(stream)))
+    return out
+
+
+def _view_of(owner: torch.Tensor, ptr, n, dtype):
+    """A cloned tensor of n elements at device address `ptr` inside the uint8 buffer `owner`."""
+    esz = torch.empty(0, dtype=dtype).element_size()
+    if n == 0:
+        return torch.empty(0, dtype=dtype, device=owner.device)
+    off = int(ptr) - owner.data_ptr()
+    assert 0 <= off and off + n * esz <= owner.numel(), "debug pointer outside its buffer"
+    return owner[off:off + n * esz].view(dtype).clone()
+
+
+def debug_tensors(layout, cams, state, arena, view):
+    """Per-view binning / pixel state copied out of the state (for parity tests)."""
+    d = debug_view(layout, cams, state, arena, view)
+    N = layout.atlas_w * layout.atlas_h
+    W, H = cams[0].width, cams[0].height
+    return {
+        "n_visible": d.n_visible, "ntiles": d.ntiles, "n_keys": d.n_keys,
+        "tile_start": _view_of(state, d.tile_start, d.ntiles, torch.int32),
+        "tile_end": _view_of(state, d.tile_end, d.ntiles, torch.int32),
+        "keys_gid": _view_of(arena, d.keys_gid, d.n_keys, torch.int32),
+        "depth_key": _view_of(state, d.depth_key, N, torch.int32),
+        "t_final": _view_of(state, d.t_final, W * H, torch.float32).reshape(H, W),
+        "n_contrib": _view_of(state, d.n_contrib, W * H, torch.int32).reshape(H, W),
+        "grad2d": _view_of(state, d.grad2d, N * 9, torch.float64).reshape(N, 9),
+        "depth_order": _view_of(state, d.depth_order, d.n_visible, torch.int32),
+    }
+
+
+# ---------------------------------------------------------------------------------------------
+# convenience: a renderer that owns state + arena and grows the arena on overflow
+
+class Renderer:
+    """Owns the per-call state and key arena for a fixed (layout, cameras) signature."""
+
+    def __init__(self, layout: Layout, cams, bg=(0.0, 0.0, 0.0), device="cuda", arena_bytes=None):
+        self.layout = layout
+        self.cams = cams
+        self.opts = opts(bg)
+        self.device = torch.device(device)
+        sb, hint = query_sizes(layout, cams, self.opts)
+        self.state = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        self.arena = torch.empty(arena_bytes if arena_bytes else hint, dtype=torch.uint8, device=self.device)
+        W, H = cams[0].width, cams[0].height
+        self.image_shape = (len(cams), 3, H, W)
+
+    def forward(self, atlas, occ, images=None, stream=None, check=True):
+        if images is None:
+            images = torch.empty(self.image_shape, dtype=torch.float32, device=self.device)
+        while True:
+            render_views(self.layout, atlas, occ, self.cams, self.opts, images, self.state, self.arena, stream)
+            if not check:
+                return images
+            ov, need = check_overflow(self.state, len(self.cams), stream)
+            if not ov:
+                return images
+            self.arena = torch.empty(int(need * 1.1) + 4096, dtype=torch.uint8, device=self.device)
+
+    def backward(self, atlas, occ, dL, grad=None, mask=None, stream=None):
+        if grad is None:
+            grad = torch.zeros_like(atlas)
+        render_backward(self.layout, atlas, occ, self.cams, self.opts, dL, mask, self.state, self.arena, grad,
+                        stream)
+        return grad

@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same
+seeded inputs.  Bit-exact for everything integer (depth keys, visibility, tile
+ranges, sorted lists, composited counts) and for the fp32-contract
+transmittance; images within 1e-4 absolute; gradients within
+max(1e-3 |g|, 1e-6) per component (BJ.north_star)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import orc
+from paper_2602_23040_b200 import puv
+from synth.scenes import Camera, Level, Scene, look_at, make_scene, tiny_scene
+from tests.gpu_common import (IMG_ATOL, describe_violations, gpu_scene, grad_violations, oracle_scene)
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(x):
+    return np.ascontiguousarray(x).view(np.uint32)
+
+
+# ---------------------------------------------------------------------------------------------
+# contract functions: GPU == oracle bit for bit
+
+def _float_range(lo, hi, stride):
+    a = np.float32(lo).view(np.uint32).astype(np.int64)
+    b = np.float32(hi).view(np.uint32).astype(np.int64)
+    return a, b
+
+
+def test_contract_exp_log_bitexact():
+    # exp_c: every fp32 in [-8, 0] (the compositing range, power in [t_g, 0]) and a 1/7 stride of
+    # bit patterns over the whole domain [-87, 88]; log_c: every fp32 in [1/255 .. 255] by stride 3
+    parts = [
+        np.arange(np.float32(0.0).view(np.uint32), np.float32(8.0).view(np.uint32) + 1, dtype=np.uint32) | 0x80000000,
+        np.arange(0, np.float32(88.0).view(np.uint32), 7, dtype=np.uint32),
+        np.arange(0, np.float32(87.0).view(np.uint32), 7, dtype=np.uint32) | 0x80000000,
+    ]
+    for op, xs in (("exp_c", np.concatenate(parts)),
+                   ("log_c", np.arange(np.float32(1e-30).view(np.uint32), np.float32(300.0).view(np.uint32), 3,
+                                       dtype=np.uint32))):
+        x = xs.view(np.float32)
+        for lo in range(0, x.size, 1 << 27):
+            chunk = x[lo:lo + (1 << 27)]
+            ref = (orc.exp_c if op == "exp_c" else orc.log_c)(chunk)
+            got = puv.debug_contract(op, torch.from_numpy(chunk).cuda()).cpu().numpy()
+            diff = _bits(got) != _bits(ref)
+            assert not diff.any(), (op, chunk[diff][:5], got[diff][:5], ref[diff][:5])
+
+
+# ---------------------------------------------------------------------------------------------
+
+def _parity_view(sc, g, planes, occ, vi, view, img_gpu, check_bins=True):
+    """Bit-exact binning / pixel state and image tolerance for one view. Returns oracle image."""
+    cam = sc.cameras[view]
+    P = orc.project(planes, occ, cam)
+    dbg = puv.debug_tensors(g["layout"], g["cams"], g["R"].state, g["R"].arena, vi)
+    ref_depth = np.where(P["visible"] == 1, P["depth_bits"], np.uint32(0xFFFFFFFF)).astype(np.uint32)
+    got_depth = dbg["depth_key"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(got_depth, ref_depth), "depth keys / visibility differ"
+    assert dbg["n_visible"] == int(P["visible"].sum())
+    if check_bins:
+        start, end, gids = orc.binning(P, cam)
+        assert dbg["n_keys"] == gids.size
+        assert np.array_equal(dbg["tile_start"].cpu().numpy().view(np.uint32), start)
+        assert np.array_equal(dbg["tile_end"].cpu().numpy().view(np.uint32), end)
+        assert np.array_equal(dbg["keys_gid"].cpu().numpy().view(np.uint32), gids), "sorted tile lists differ"
+    ref_img, T, nc, st = orc.forward(planes, occ, sc.sh_degree, cam)
+    assert np.array_equal(_bits(dbg["t_final"].cpu().numpy()), _bits(T)), "T_final differs"
+    assert np.array_equal(dbg["n_contrib"].cpu().numpy(), nc), "n_contrib differs"
+    err = np.abs(img_gpu - ref_img).max()
+    assert err <= IMG_ATOL, err
+    return ref_img
+
+
+def _grad_check(sc, planes, occ, views, dls_ref, grad_gpu, mask=None, bg=(0.0, 0.0, 0.0)):
+    g_ref = np.zeros(planes.shape, np.float64)
+    for v, dl in zip(views, dls_ref):
+        orc.backward(planes, occ, sc.sh_degree, sc.cameras[v], dl, mask=mask, bg=bg, grad=g_ref)
+    bad = grad_violations(grad_gpu, g_ref)
+    frac = bad.mean()
+    assert not bad.any(), f"{bad.sum()} of {bad.size} components ({frac:.2e}) outside tolerance: " + \
+        describe_violations(grad_gpu, g_ref, bad)
+    return g_ref
+
+
+def _run(sc, views, dls=None, bg=(0.0, 0.0, 0.0), mask=None, arena_bytes=None):
+    """GPU forward (+ its own L2 loss) and backward.  The backward consumes `dls` (the oracle's
+    dL/dImage, fp64 -> fp32) when given, so gradient parity compares the two backwards on the
+    same input; otherwise the GPU's own dL."""
+    g = gpu_scene(sc, views, bg=bg, arena_bytes=arena_bytes)
+    img = g["R"].forward(g["atlas"], g["occ"])
+    tg = torch.from_numpy(np.stack([sc.target(v) for v in g["views"]])).cuda()
+    dL = torch.empty_like(img)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    puv.l2_loss_grad(img, tg, dL, loss)
+    if dls is not None:
+        dL = torch.from_numpy(np.stack(dls).astype(np.float32)).cuda()
+    m = None if mask is None else torch.from_numpy(mask).cuda()
+    grad = g["R"].backward(g["atlas"], g["occ"], dL, mask=m)
+    torch.cuda.synchronize()
+    return g, img.cpu().numpy(), loss.item(), grad.cpu().numpy()
+
+
+def _oracle_dls(sc, planes, occ, views, bg=(0.0, 0.0, 0.0)):
+    """Oracle images and dL/dImage = I_hat - I (R11), rounded to the fp32 the GPU consumes."""
+    imgs, dls = [], []
+    for v in views:
+        ref = orc.forward(planes, occ, sc.sh_degree, sc.cameras[v], bg=bg)[0]
+        imgs.append(ref)
+        dls.append(orc.l2_loss_grad(ref, sc.target(v))[1].astype(np.float32).astype(np.float64))
+    return imgs, dls
+
+
+def test_c1_full_parity():
+    sc = make_scene(1)
+    planes, occ, _ = oracle_scene(sc)
+    refs, dls = _oracle_dls(sc, planes, occ, [0])
+    g, img, loss, grad = _run(sc, [0], dls=dls)
+    assert np.array_equal(_bits(g["atlas"].cpu().numpy()), _bits(planes)), "pack differs"
+    _parity_view(sc, g, planes, occ, 0, 0, img[0])
+    L_ref = orc.l2_loss_grad(refs[0], sc.target(0))[0]
+    assert abs(loss - L_ref) <= 1e-6 * L_ref
+    _grad_check(sc, planes, occ, [0], dls, grad)
+
+
+def test_c2_parity_two_views():
+    sc = make_scene(2)
+    views = [0, 5]
+    planes, occ, _ = oracle_scene(sc)
+    refs, dls = _oracle_dls(sc, planes, occ, views)
+    g, img, loss, grad = _run(sc, views, dls=dls)
+    assert np.array_equal(_bits(g["atlas"].cpu().numpy()), _bits(planes))
+    assert np.array_equal(g["occ"].cpu().numpy(), occ)
+    for vi, v in enumerate(views):
+        _parity_view(sc, g, planes, occ, vi, v, img[vi])
+    _grad_check(sc, planes, occ, views, dls, grad)
+
+
+def test_edge_ragged_multiview_empty_views_bg_mask():
+    """Ragged image (100x75, partial tiles), 18 views (> one camera batch), views that see nothing,
+    a background colour and a dynamic mask."""
+    rng = np.random.default_rng(7)
+    n = 37 * 23
+    mu = rng.uniform(-1, 1, (n, 3))
+    sh = np.concatenate([rng.random((n, 3)), rng.normal(0, 0.1, (n, 9))], axis=1)
+    cams = []
+    for i in range(18):
+        a = 2 * math.pi * i / 18
+        if i in (4, 11):   # looking away from the scene: nothing visible
+            cams.append(look_at((3 * math.cos(a), 3 * math.sin(a), 0.5), (6 * math.cos(a), 6 * math.sin(a), 0.5),
+                                100, 75, 80.0))
+        else:
+            cams.append(look_at((3 * math.cos(a), 3 * math.sin(a), 0.5), (0, 0, 0), 100, 75, 80.0))
+    sc = tiny_scene(mu, [-2.5] * 3, [1, 0, 0, 0], rng.normal(0, 1, n), sh, cams[0], 1)
+    lv = sc.levels[0]
+    lv.planes[3:6] = rng.normal(-2.6, 0.4, (3, 1, n)).astype(np.float32)
+    lv.planes[6:10] = rng.normal(size=(4, 1, n)).astype(np.float32)
+    lv.occ[0, ::13] = 0    # holes
+    # reshape the 1 x n level into 37 x 23 so the atlas is 2-D
+    sc.levels = [Level(planes=np.ascontiguousarray(lv.planes.reshape(-1, 37, 23)),
+                       occ=np.ascontiguousarray(lv.occ.reshape(37, 23)),
+                       labels=np.ascontiguousarray(lv.labels.reshape(37, 23)))]
+    sc.cameras = cams
+    sc.cfg = 99
+    bg = (0.25, 0.5, 0.75)
+    mask = (rng.random((37, 23)) < 0.5).astype(np.uint8)
+    views = list(range(18))
+    planes, occ, _ = oracle_scene(sc)
+    _, dls = _oracle_dls(sc, planes, occ, views, bg=bg)
+    g, img, loss, grad = _run(sc, views, dls=dls, bg=bg, mask=mask)
+    for vi in views:
+        cam = sc.cameras[vi]
+        P = orc.project(planes, occ, cam)
+        ref, T, nc, st = orc.forward(planes, occ, 1, cam, bg=bg)
+        dbg = puv.debug_tensors(g["layout"], g["cams"], g["R"].state, g["R"].arena, vi)
+        start, end, gids = orc.binning(P, cam)
+        assert np.array_equal(dbg["keys_gid"].cpu().numpy().view(np.uint32), gids)
+        assert np.array_equal(dbg["tile_start"].cpu().numpy().view(np.uint32), start)
+        assert np.array_equal(dbg["n_contrib"].cpu().numpy(), nc)
+        assert np.array_equal(_bits(dbg["t_final"].cpu().numpy()), _bits(T))
+        assert np.abs(img[vi] - ref).max() <= IMG_ATOL
+        if vi in (4, 11):
+            assert st["n_vis"] == 0 and dbg["n_keys"] == 0
+            assert np.allclose(img[vi], np.array(bg)[:, None, None])
+    _grad_check(sc, planes, occ, views, dls, grad, mask=mask, bg=bg)
+    assert np.all(grad[:, mask == 0] == 0)
+
+
+def test_arena_overflow_flag_and_retry():
+    sc = make_scene(1)
+    g = gpu_scene(sc, [0], arena_bytes=4096)
+    R = g["R"]
+    img = torch.empty(R.image_shape, dtype=torch.float32, device="cuda")
+    puv.render_views(R.layout, g["atlas"], g["occ"], R.cams, R.opts, img, R.state, R.arena)
+    ov, need = puv.check_overflow(R.state, 1)
+    planes, occ, _ = oracle_scene(sc)
+    P = orc.project(planes, occ, sc.cameras[0])
+    K = int(P["tiles"][P["visible"] == 1].sum())
+    assert ov and need == 4 * K
+    assert torch.all(img == 0)     # overflowed view renders only the (black) background
+    img2 = R.forward(g["atlas"], g["occ"])   # grows the arena and re-renders
+    assert R.arena.numel() >= 4 * K
+    ref, _, _, _ = orc.forward(planes, occ, 0, sc.cameras[0])
+    assert np.abs(img2.cpu().numpy()[0] - ref).max() <= IMG_ATOL
+
+
+def test_pack_rotated_levels_and_unpack_roundtrip():
+    rng = np.random.default_rng(3)
+    D = 14
+    lv = [Level(planes=rng.random((D, 5, 3)).astype(np.float32), occ=np.ones((5, 3), np.uint8),
+                labels=np.ones((5, 3), np.uint8)),
+          Level(planes=rng.random((D, 2, 4)).astype(np.float32), occ=(rng.random((2, 4)) < 0.5).astype(np.uint8),
+                labels=np.ones((2, 4), np.uint8))]
+    place = np.array([[0, 0, 1], [5, 0, 0]], np.int32)   # level 0 rotated: 3 tall x 5 wide
+    ref_planes, ref_occ, _ = orc.pack(lv, place=place, W=9, H=3)
+    layout = puv.layout_for_levels([(5, 3), (2, 4)], 0)
+    layout.atlas_w, layout.atlas_h = 9, 3
+    for k, (x, y, r) in enumerate(place):
+        layout.level[k].x, layout.level[k].y, layout.level[k].rot90ccw = int(x), int(y), int(r)
+    atlas, occ = puv.pack_atlas(layout, [torch.from_numpy(l.planes).cuda() for l in lv],
+                                [torch.from_numpy(l.occ).cuda() for l in lv])
+    assert np.array_equal(atlas.cpu().numpy(), ref_planes) and np.array_equal(occ.cpu().numpy(), ref_occ)
+    back = puv.unpack_levels(layout, atlas)
+    for b, l in zip(back, lv):
+        assert np.array_equal(b.cpu().numpy(), l.planes)
+
+
+@pytest.mark.slow
+def test_c3_full_size_parity_views_0_33():
+    """C3 at full size in the bench's launch configuration (all 64 views in one call);
+    bit-exact binning and pixel state + image tolerance on views 0 and 33; gradients of
+    a 2-view call against the oracle's."""
+    sc = make_scene(3)
+    g = gpu_scene(sc, None)
+    img = g["R"].forward(g["atlas"], g["occ"])
+    torch.cuda.synchronize()
+    planes, occ, _ = oracle_scene(sc)
+    imgs = img.cpu().numpy()
+    for v in (0, 33):
+        _parity_view(sc, g, planes, occ, v, v, imgs[v])
+    del g, img
+    torch.cuda.empty_cache()
+    views = [0, 33]
+    _, dls = _oracle_dls(sc, planes, occ, views)
+    g, img2, loss, grad = _run(sc, views, dls=dls)
+    _grad_check(sc, planes, occ, views, dls, grad)

@@ -160,10 +160,38 @@ typedef struct {
   const uint32_t* n_contrib;     /* device, H*W: list position after the last composited entry */
   const double* grad2d;          /* device, H_A*W_A*9 fp64: per-Gaussian 2D grads (mx,my,ha,nb,hc,o,r,g,b) of the last backward */
   const uint32_t* depth_order;   /* device, n_visible gids sorted by (depth_bits, gid) */
+  uint64_t n_examined;           /* (pixel, entry) pairs that ran the skip test in the forward */
+  uint64_t n_composited;         /* pairs composited in the forward */
 } puv_view_debug;
 
 puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, const void* state,
                           size_t state_bytes, const void* arena, int32_t view, void* stream, puv_view_debug* out);
+
+/* Stage profiling.  When enabled, every library call records a CUDA event pair
+ * around each stage on the call's stream (asynchronous, no host sync).
+ * puv_profile_read synchronises those events and returns, per stage, the summed
+ * device milliseconds, the kernels launched and the number of timed stage
+ * instances; kernel_launches counts every kernel the library launched since it
+ * was loaded (profiling on or off).  Stages: */
+#define PUV_NUM_STAGES 8
+enum {
+  PUV_STAGE_PROJECT = 0,      /* K1 unpack + EWA projection + SH colour + rect (rows a1, a2) */
+  PUV_STAGE_DEPTH_SORT = 1,   /* K3 depth radix sort with culling compaction (row a4, low digit) */
+  PUV_STAGE_BIN = 2,          /* K2/K4 key generation + stable tile pass + tile ranges (rows a3, a4) */
+  PUV_STAGE_RASTER_FWD = 3,   /* K5 composite (row a5) */
+  PUV_STAGE_LOSS = 4,         /* K10 L2 loss gradient (row a6) */
+  PUV_STAGE_RASTER_BWD = 5,   /* K6 composite backward (row a7) */
+  PUV_STAGE_PROJECT_BWD = 6,  /* K7 projection + unpack backward, scatter to texels (rows a8, a9) */
+  PUV_STAGE_PACK = 7          /* K9 pack / unpack */
+};
+typedef struct {
+  double ms[PUV_NUM_STAGES];
+  uint64_t launches[PUV_NUM_STAGES];
+  uint64_t calls[PUV_NUM_STAGES];
+  uint64_t kernel_launches;
+} puv_profile;
+puv_status puv_profile_enable(int32_t on);
+puv_status puv_profile_read(puv_profile* out, int32_t reset);
 
 /* Evaluate a contract function of DESIGN.md R13 elementwise on device arrays (for the
  * exhaustive GPU-vs-oracle bit-equality test).  op: 0 = exp_c, 1 = log_c.  in/out: device, n floats. */

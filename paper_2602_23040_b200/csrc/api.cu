@@ -7,6 +7,9 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <atomic>
+#include <mutex>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -17,6 +20,45 @@
 namespace puv {
 
 static thread_local std::string g_err;
+
+// ---- launch accounting and stage profiling ------------------------------------------------------
+static std::atomic<uint64_t> g_launches{0};
+void count_launches(int n) { g_launches += (uint64_t)n; }
+
+struct ProfEvent { int stage; cudaEvent_t a, b; uint64_t launches; };
+static std::mutex g_prof_mu;
+static std::atomic<bool> g_prof_on{false};
+static std::vector<ProfEvent> g_prof_events;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) { cudaEvent_t e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII: records an event pair around one stage on `s` when profiling is on.
+struct StageScope {
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  uint64_t l0 = 0;
+  StageScope(int st, cudaStream_t stream) : stage(st), s(stream) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    a = take_event();
+    cudaEventRecord(a, s);
+    l0 = g_launches;
+  }
+  ~StageScope() {
+    if (!a) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = take_event();
+    cudaEventRecord(b, s);
+    g_prof_events.push_back({stage, a, b, g_launches - l0});
+  }
+};
 
 static puv_status fail(puv_status code, const char* fmt, ...) {
   char buf[512];
@@ -229,7 +271,8 @@ puv_status puv_pack_atlas(const puv_layout* layout, const float* const* level_pl
     if (!level_planes[i]) return fail(PUV_E_INVALID_ARGUMENT, "level plane %d is NULL", i);
   for (int d = 0; d < layout->planes; ++d)
     if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
-  launch_pack(*layout, level_planes, level_occ, atlas_planes, atlas_occ, (cudaStream_t)stream);
+  { StageScope sc(PUV_STAGE_PACK, (cudaStream_t)stream);
+    launch_pack(*layout, level_planes, level_occ, atlas_planes, atlas_occ, (cudaStream_t)stream); }
   return cuda_check("puv_pack_atlas");
 }
 
@@ -238,7 +281,8 @@ puv_status puv_unpack_levels(const puv_layout* layout, const float* const* atlas
   puv_status st = check_layout(layout);
   if (st) return st;
   if (!level_planes || !atlas_planes) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer table");
-  launch_unpack(*layout, atlas_planes, level_planes, (cudaStream_t)stream);
+  { StageScope sc(PUV_STAGE_PACK, (cudaStream_t)stream);
+    launch_unpack(*layout, atlas_planes, level_planes, (cudaStream_t)stream); }
   return cuda_check("puv_unpack_levels");
 }
 
@@ -268,18 +312,21 @@ puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_
   const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
   cudaStream_t s = (cudaStream_t)stream;
   const Plan& p = c.plan;
+  cudaMemsetAsync(c.views.hdr, 0, sizeof(ViewHdr) * n_views, s);
   launch_begin_call(p, c.views, arena_bytes / 4, s);
   for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
     CamBatch cb;
     cb.v0 = v0;
     cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
     for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
+    StageScope sc(PUV_STAGE_PROJECT, s);
     launch_project(p, c.views, c.P, atlas_occ, cb, s);
   }
   for (int v = 0; v < n_views; ++v) {
-    launch_depth_sort(p, c.views, state, v, s);
-    launch_bin(p, c.views, state, (uint32_t*)arena, v, s);
-    launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)v * 3 * p.HW, v, bg, s);
+    { StageScope sc(PUV_STAGE_DEPTH_SORT, s); launch_depth_sort(p, c.views, state, v, s); }
+    { StageScope sc(PUV_STAGE_BIN, s); launch_bin(p, c.views, state, (uint32_t*)arena, v, s); }
+    { StageScope sc(PUV_STAGE_RASTER_FWD, s);
+      launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)v * 3 * p.HW, v, bg, s); }
   }
   return cuda_check("puv_render_views");
 }
@@ -288,7 +335,8 @@ puv_status puv_l2_loss_grad(int64_t n, const float* images, const float* targets
                             void* stream) {
   if (n < 0 || (n > 0 && (!images || !targets || !dL_dimages)) || !loss)
     return fail(PUV_E_INVALID_ARGUMENT, "bad loss arguments");
-  launch_l2_loss(n, images, targets, dL_dimages, loss, (cudaStream_t)stream);
+  { StageScope sc(PUV_STAGE_LOSS, (cudaStream_t)stream);
+    launch_l2_loss(n, images, targets, dL_dimages, loss, (cudaStream_t)stream); }
   return cuda_check("puv_l2_loss_grad");
 }
 
@@ -309,12 +357,14 @@ puv_status puv_render_backward(const puv_layout* layout, const float* const* atl
   cudaStream_t s = (cudaStream_t)stream;
   const Plan& p = c.plan;
   for (int v = 0; v < n_views; ++v)
-    launch_raster_bwd(p, c.views, (const uint32_t*)arena, dL_dimages + (size_t)v * 3 * p.HW, v, bg, s);
+  { StageScope sc(PUV_STAGE_RASTER_BWD, s);
+    launch_raster_bwd(p, c.views, (const uint32_t*)arena, dL_dimages + (size_t)v * 3 * p.HW, v, bg, s); }
   for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
     CamBatch cb;
     cb.v0 = v0;
     cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
     for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
+    StageScope sc(PUV_STAGE_PROJECT_BWD, s);
     launch_project_bwd(p, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s);
   }
   return cuda_check("puv_render_backward");
@@ -362,6 +412,8 @@ puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_c
   out->n_contrib = v.ncontrib + (size_t)view * p.HW;
   out->grad2d = v.grad2d + (size_t)view * p.N * 9;
   out->depth_order = v.sorted + (size_t)view * p.N;
+  out->n_examined = h.examined;
+  out->n_composited = h.composited;
   return PUV_OK;
 }
 
@@ -369,6 +421,32 @@ puv_status puv_debug_contract(int32_t op, const float* in, float* out, int64_t n
   if ((op != 0 && op != 1) || n < 0 || (n > 0 && (!in || !out))) return fail(PUV_E_INVALID_ARGUMENT, "bad contract args");
   if (n) launch_contract(op, in, out, n, (cudaStream_t)stream);
   return cuda_check("puv_debug_contract");
+}
+
+puv_status puv_profile_enable(int32_t on) {
+  g_prof_on = on != 0;
+  return PUV_OK;
+}
+
+puv_status puv_profile_read(puv_profile* out, int32_t reset) {
+  if (!out) return fail(PUV_E_INVALID_ARGUMENT, "NULL profile");
+  std::memset(out, 0, sizeof *out);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (const ProfEvent& e : g_prof_events) {
+    const cudaError_t err = cudaEventSynchronize(e.b);
+    if (err != cudaSuccess) return fail(PUV_E_CUDA, "puv_profile_read: %s", cudaGetErrorString(err));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    out->ms[e.stage] += ms;
+    out->launches[e.stage] += e.launches;
+    out->calls[e.stage] += 1;
+  }
+  if (reset) {
+    for (const ProfEvent& e : g_prof_events) { g_event_pool.push_back(e.a); g_event_pool.push_back(e.b); }
+    g_prof_events.clear();
+  }
+  out->kernel_launches = g_launches;
+  return PUV_OK;
 }
 
 size_t puv_last_error(char* buf, size_t len) {

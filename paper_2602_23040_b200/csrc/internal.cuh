@@ -36,7 +36,10 @@ struct ViewHdr {
   uint64_t list_base;     // offset (in keys) of this view's lists inside the arena
   uint32_t kb;            // keys per block of the stable tile pass
   uint32_t nb;            // blocks of the stable tile pass
-  uint64_t pad[4];
+  uint64_t ktotal;        // scratch: K before the arena is carved
+  uint64_t examined;      // (pixel, entry) pairs that ran the skip test in K5
+  uint64_t composited;    // pairs composited in K5
+  uint64_t pad;
 };
 struct CallHdr {
   uint64_t arena_used;    // keys handed out so far (running sum over views)
@@ -81,6 +84,9 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 Plan make_plan(const puv_layout& L, int n_views, int W, int H);
 Views views_of(const Plan& p, void* state);
+
+// ---- launch accounting (every kernel launch of the library is counted; see puv_profile_read) ----
+void count_launches(int n);
 
 // ---- launchers (all asynchronous on `s`) ----
 void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,

@@ -384,7 +384,7 @@ void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int
   uint32_t* bsum = (uint32_t*)(st + p.bsum);
   uint32_t* koff = (uint32_t*)(st + p.koff);
   uint32_t* cnt = (uint32_t*)(st + p.cnt);
-  uint64_t* ktot = &hdr->pad[0];  // scratch: K of this view before finalize
+  uint64_t* ktot = &hdr->ktotal;  // scratch: K of this view before finalize
   uint32_t* tstart = v.tstart + (size_t)view * p.ntiles;
   uint32_t* tend = v.tend + (size_t)view * p.ntiles;
   const int nsb = p.N / kScanTile + 1;   // one extra block so koff[n_vis] (= K) is always written
@@ -412,6 +412,7 @@ void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int
     k_tile_scatter<false><<<2 * nsm, kBinThreads, sc_smem, s>>>(hdr, koff, sorted, rect, p.gx, p.ntiles, cnt, tstart,
                                                                 arena);
   }
+  count_launches(8);
 }
 
 }  // namespace puv

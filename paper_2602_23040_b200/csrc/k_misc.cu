@@ -45,6 +45,7 @@ void launch_pack(const puv_layout& L, const float* const* level_planes, const ui
     k_pack_level<<<(n + 255) / 256, 256, 0, s>>>(src, level_occ ? level_occ[k] : nullptr, dst, atlas_occ, L.planes,
                                                  pl.rows, pl.cols, pl.x, pl.y, pl.rot90ccw, L.atlas_w);
   }
+  count_launches(L.num_levels);
 }
 
 void launch_unpack(const puv_layout& L, const float* const* atlas_planes, float* const* level_planes, cudaStream_t s) {
@@ -58,6 +59,7 @@ void launch_unpack(const puv_layout& L, const float* const* atlas_planes, float*
     k_unpack_level<<<(n + 255) / 256, 256, 0, s>>>(dst, src, L.planes, pl.rows, pl.cols, pl.x, pl.y, pl.rot90ccw,
                                                    L.atlas_w);
   }
+  count_launches(L.num_levels);
 }
 
 // L = 1/2 sum (img - tgt)^2 ; dl = img - tgt.  float4 vectorised, fp64 partial sums.
@@ -102,6 +104,7 @@ void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, do
   const int blocks = (int)(want < 4 * nsm ? (want > 0 ? want : 1) : 4 * nsm);
   const bool vec = ((uintptr_t)img % 16 == 0) && ((uintptr_t)tgt % 16 == 0) && ((uintptr_t)dl % 16 == 0);
   k_l2_loss<<<blocks, 256, 0, s>>>(n, img, tgt, dl, loss, vec);
+  count_launches(1);
 }
 
 __global__ void k_contract(int op, const float* __restrict__ in, float* __restrict__ out, int64_t n) {
@@ -111,6 +114,7 @@ __global__ void k_contract(int op, const float* __restrict__ in, float* __restri
 
 void launch_contract(int op, const float* in, float* out, int64_t n, cudaStream_t s) {
   k_contract<<<1184, 256, 0, s>>>(op, in, out, n);
+  count_launches(1);
 }
 
 __global__ void k_begin_call(CallHdr* call, uint64_t cap) {
@@ -122,6 +126,7 @@ __global__ void k_begin_call(CallHdr* call, uint64_t cap) {
 
 void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaStream_t s) {
   k_begin_call<<<1, 1, 0, s>>>(v.call, arena_cap);
+  count_launches(1);
 }
 
 }  // namespace puv

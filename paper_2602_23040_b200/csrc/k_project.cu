@@ -94,6 +94,7 @@ void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint
     case 2: k_project<2><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
     default: k_project<3><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
   }
+  count_launches(1);
 }
 
 }  // namespace puv

@@ -177,6 +177,7 @@ void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const 
     case 2: k_project_bwd<2><<<blocks, threads, 0, s>>>(P, occ, mask, p.N, cb, v, G); break;
     default: k_project_bwd<3><<<blocks, threads, 0, s>>>(P, occ, mask, p.N, cb, v, G); break;
   }
+  count_launches(1);
 }
 
 }  // namespace puv

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
   const float4* rec = v.rec + (size_t)view * N * 3;
   const float fi = (float)px, fj = (float)py;
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  uint32_t last = 0;
+  uint32_t last = 0, n_exam = 0, n_comp = 0;
   bool done = !inside;
   for (uint32_t b0 = start; b0 < end; b0 += kRasterThreads) {
     if (__syncthreads_count(done) == kRasterThreads) break;
@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
       const float4 A = sA[j];
       const float4 B = sB[j];
       const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi, fj);
+      ++n_exam;
       if (power > 0.0f || power < B.y) continue;
       const float ao = mul(B.z, exp_c(power));
       const float alpha = ao < 0.99f ? ao : 0.99f;
@@ -69,6 +70,14 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
       C2 = fmaf(Cc.z, w, C2);
       T = Tn;
       last = b0 + j + 1 - start;
+      ++n_comp;
+    }
+  }
+  {  // pair statistics (one atomic per warp)
+    const uint32_t we = __reduce_add_sync(0xffffffffu, n_exam), wc = __reduce_add_sync(0xffffffffu, n_comp);
+    if ((threadIdx.x & 31) == 0 && (we | wc)) {
+      atomicAdd((unsigned long long*)&v.hdr[view].examined, (unsigned long long)we);
+      atomicAdd((unsigned long long*)&v.hdr[view].composited, (unsigned long long)wc);
     }
   }
   if (inside) {
@@ -86,6 +95,7 @@ void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, flo
                        const float bg[3], cudaStream_t s) {
   k_raster_fwd<<<p.ntiles, kRasterThreads, 0, s>>>(arena, v, view, p.N, p.W, p.H, p.gx, p.ntiles, bg[0], bg[1], bg[2],
                                                    image);
+  count_launches(1);
 }
 
 }  // namespace puv

@@ -183,6 +183,7 @@ void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, con
                        const float bg[3], cudaStream_t s) {
   k_raster_bwd<<<p.ntiles, kBwdThreads, 0, s>>>(arena, v, view, p.N, p.W, p.H, p.gx, p.ntiles, bg[0], bg[1], bg[2],
                                                 dL_dimage);
+  count_launches(1);
 }
 
 }  // namespace puv

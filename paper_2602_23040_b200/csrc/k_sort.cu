@@ -157,6 +157,7 @@ void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cud
     k_radix_downsweep<false><<<nb, kSortThreads, 0, s>>>(ki[pass - 1], vi[pass - 1], ko[pass - 1], vo[pass - 1], nvis,
                                                           0, sh, hist, nb);
   }
+  count_launches(12);
 }
 
 }  // namespace puv

@@ -56,7 +56,16 @@ class ViewDebug(C.Structure):
                 ("tiles_y", C.c_uint32), ("n_keys", C.c_uint64), ("tile_start", C.c_void_p),
                 ("tile_end", C.c_void_p), ("keys_gid", C.c_void_p), ("depth_key", C.c_void_p),
                 ("t_final", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
-                ("depth_order", C.c_void_p)]
+                ("depth_order", C.c_void_p), ("n_examined", C.c_uint64), ("n_composited", C.c_uint64)]
+
+
+NUM_STAGES = 8
+STAGES = ("project", "depth_sort", "bin", "raster_fwd", "loss", "raster_bwd", "project_bwd", "pack")
+
+
+class Profile(C.Structure):
+    _fields_ = [("ms", C.c_double * NUM_STAGES), ("launches", C.c_uint64 * NUM_STAGES),
+                ("calls", C.c_uint64 * NUM_STAGES), ("kernel_launches", C.c_uint64)]
 
 
 _LIB = None
@@ -80,6 +89,10 @@ def lib():
         L.puv_check_overflow.argtypes = [P, S, P, P, P]
         L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
         L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
+        L.puv_profile_enable.argtypes = [S]
+        L.puv_profile_read.argtypes = [P, S]
+        L.puv_profile_enable.restype = C.c_int32
+        L.puv_profile_read.restype = C.c_int32
         L.puv_last_error.argtypes = [C.c_char_p, C.c_size_t]
         L.puv_last_error.restype = C.c_size_t
         L.puv_version.restype = C.c_char_p
@@ -220,6 +233,26 @@ def debug_view(layout, cams, state, arena, view, stream=None) -> ViewDebug:
     return out
 
 
+def profile_enable(on: bool = True):
+    _ok(lib().puv_profile_enable(1 if on else 0))
+
+
+def profile_read(reset: bool = True) -> dict:
+    """Per-stage device ms / kernel launches / stage instances since the last reset (syncs)."""
+    p = Profile()
+    _ok(lib().puv_profile_read(C.byref(p), 1 if reset else 0))
+    return {"ms": {s: p.ms[i] for i, s in enumerate(STAGES)},
+            "launches": {s: int(p.launches[i]) for i, s in enumerate(STAGES)},
+            "calls": {s: int(p.calls[i]) for i, s in enumerate(STAGES)},
+            "kernel_launches": int(p.kernel_launches)}
+
+
+def kernel_launches() -> int:
+    p = Profile()
+    _ok(lib().puv_profile_read(C.byref(p), 0))
+    return int(p.kernel_launches)
+
+
 def debug_contract(op: str, x: torch.Tensor, stream=None) -> torch.Tensor:
     """exp_c / log_c of DESIGN.md R13 on a CUDA fp32 tensor (bit-equality tests)."""
     out = torch.empty_like(x)
@@ -244,6 +277,7 @@ def debug_tensors(layout, cams, state, arena, view):
     W, H = cams[0].width, cams[0].height
     return {
         "n_visible": d.n_visible, "ntiles": d.ntiles, "n_keys": d.n_keys,
+        "n_examined": d.n_examined, "n_composited": d.n_composited,
         "tile_start": _view_of(state, d.tile_start, d.ntiles, torch.int32),
         "tile_end": _view_of(state, d.tile_end, d.ntiles, torch.int32),
         "keys_gid": _view_of(arena, d.keys_gid, d.n_keys, torch.int32),

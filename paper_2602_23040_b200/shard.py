@@ -1,0 +1,55 @@
+"""View sharding over torch.distributed (row a10 of DESIGN.md §1).
+
+Cameras shard naturally across GPUs (BJ.north_star): rank r renders views
+v = r, r + n, r + 2n, ... (round-robin mixes the two camera rings of C3 so the
+per-rank key counts balance), accumulates its local atlas gradient with
+`render_backward` (+=), and the gradient planes are summed with ONE
+all-reduce over NCCL (NVLink 5 / NVSwitch).  The atlas is replicated.  The
+loss is summed the same way.  Everything here is orchestration: the render
+runs in libpuv's kernels.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import puv
+
+
+def local_views(n_views: int, rank: int, world: int) -> list[int]:
+    return [v for v in range(n_views) if v % world == rank]
+
+
+class ShardedStep:
+    """One fwd + loss + bwd step over this rank's views, then the gradient all-reduce."""
+
+    def __init__(self, layout, cameras, rank=0, world=1, device="cuda", bg=(0.0, 0.0, 0.0), arena_bytes=None,
+                 group=None):
+        self.rank, self.world, self.group = rank, world, group
+        self.views = local_views(len(cameras), rank, world)
+        if not self.views:
+            raise ValueError(f"rank {rank} of {world} has no views (n_views={len(cameras)})")
+        self.device = torch.device(device)
+        self.cams = puv.cameras([cameras[v] for v in self.views])
+        self.R = puv.Renderer(layout, self.cams, bg=bg, device=self.device, arena_bytes=arena_bytes)
+        self.images = torch.empty(self.R.image_shape, dtype=torch.float32, device=self.device)
+        self.dL = torch.empty_like(self.images)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+
+    def step(self, atlas, occ, targets, grad, mask=None, check_overflow=False):
+        """targets: (n_local, 3, H, W) fp32 on device; grad: (D, H_A, W_A) fp32, zeroed by the caller.
+        Returns the (device) loss, summed over ranks when world > 1."""
+        if check_overflow:
+            self.R.forward(atlas, occ, images=self.images, check=True)
+        else:
+            puv.render_views(self.R.layout, atlas, occ, self.cams, self.R.opts, self.images, self.R.state,
+                             self.R.arena)
+        puv.l2_loss_grad(self.images, targets, self.dL, self.loss)
+        self.R.backward(atlas, occ, self.dL, grad=grad, mask=mask)
+        if self.world > 1:
+            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(self.loss, op=dist.ReduceOp.SUM, group=self.group)
+        return self.loss
+
+    def overflowed(self) -> bool:
+        return puv.check_overflow(self.R.state, len(self.views))[0]

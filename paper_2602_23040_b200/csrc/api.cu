@@ -167,12 +167,13 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.tend = take(4 * V * p.ntiles);
   p.tfinal = take(4 * V * p.HW);
   p.ncontrib = take(4 * V * p.HW);
+  p.cfull = take(24 * V * p.HW);
   p.sort_blocks = (N + 2047) / 2048;
   p.sk0 = take(4 * N);
   p.sv0 = take(4 * N);
   p.sk1 = take(4 * N);
   p.sv1 = take(4 * N);
-  p.hist = take(4 * 256 * p.sort_blocks);
+  p.hist = take(depth_sort_scratch_bytes(N));
   p.koff = take(4 * (N + 1));
   p.bsum = take(4 * (N / 2048 + 2));
   p.cnt = take(4 * (size_t)kNbMax * p.ntiles);
@@ -193,6 +194,7 @@ Views views_of(const Plan& p, void* state) {
   v.tend = (uint32_t*)(s + p.tend);
   v.tfinal = (float*)(s + p.tfinal);
   v.ncontrib = (uint32_t*)(s + p.ncontrib);
+  v.cfull = (double*)(s + p.cfull);
   v.hdr = (ViewHdr*)(s + p.view_hdr);
   v.call = (CallHdr*)(s + p.call_hdr);
   return v;

@@ -69,4 +69,32 @@ PUV_DEV float pair_power(float mx, float my, float ha, float nb, float hc, float
   return fma_(dx, u, mul(mul(hc, dy), dy));
 }
 
+// ---- fp64 exp for the value path (not part of the contract) ----------------------------------
+// exp(x) = 2^m * 2^(j/64) * e^r,  k = rint(64 x / ln2) = 64 m + j,  |r| <= ln2/128,
+// e^r by its degree-5 Taylor polynomial (truncation < 4e-17).  `tab` = 2^(j/64), j < 64,
+// staged in shared memory by the caller (exp64_table_fill).  Valid for x in [-700, 0].
+PUV_DEV void exp64_table_fill(double* tab) {
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = exp2((double)j / 64.0);
+}
+
+PUV_DEV double exp64(double x, const double* tab) {
+  constexpr double kInvL = 92.33248261689366;            // 64 / ln 2
+  constexpr double kLhi = 0.010830424696223417;          // ln2/64 high part (trailing bits zero)
+  constexpr double kLlo = 2.572804622327669e-14;         // ln2/64 - kLhi
+  constexpr double kShift = 6755399441055744.0;          // 1.5 * 2^52: rint by addition
+  const double t = fma(x, kInvL, kShift);
+  const int k = (int)__double2loint(t);                  // low word = rint(64 x / ln2) (two's complement)
+  const double kd = t - kShift;
+  double r = fma(-kd, kLhi, x);
+  r = fma(-kd, kLlo, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(r, p, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r, p, 1.0);
+  p = fma(r, p, 1.0);
+  const double v = tab[k & 63] * p;
+  const int m = k >> 6;                                  // arithmetic shift: floor(k / 64)
+  return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
+}
+
 }  // namespace puv

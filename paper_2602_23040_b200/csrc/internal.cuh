@@ -55,7 +55,7 @@ struct Plan {
   int n_views, N, W, H, HW, gx, gy, ntiles, D, deg;
   size_t call_hdr, view_hdr;
   // per view arrays, each [n_views][...]
-  size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib;
+  size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull;
   // scratch shared by all views (reused in stream order)
   size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt;
   size_t sort_blocks;      // blocks of one radix pass over N items
@@ -76,6 +76,7 @@ struct Views {
   uint32_t* tend;    // [V][ntiles]
   float* tfinal;     // [V][HW]
   uint32_t* ncontrib;// [V][HW]
+  double* cfull;     // [V][HW][3]  fp64 full colour sum c a T + T_final bg (forward -> backward)
   ViewHdr* hdr;      // [V]
   CallHdr* call;
 };
@@ -87,6 +88,7 @@ Views views_of(const Plan& p, void* state);
 
 // ---- launch accounting (every kernel launch of the library is counted; see puv_profile_read) ----
 void count_launches(int n);
+size_t depth_sort_scratch_bytes(size_t N);
 
 // ---- launchers (all asynchronous on `s`) ----
 void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,

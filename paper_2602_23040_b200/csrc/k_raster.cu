@@ -2,16 +2,16 @@
 //
 // One 256-thread block per 16x16 tile, one pixel per thread (PAPER.md:195
 // "tile-based rasterizer"; semantics R9).  The tile's sorted Gaussian list is
-// consumed in batches of 256: each thread gathers one record into shared
-// memory (float4 x3 per entry, LDS.128 broadcast on use).  A warp stops
-// walking a batch as soon as all its pixels have terminated (ballot), the
-// block stops fetching batches once all 256 pixels have (syncthreads_count).
-// The skip test, alpha, cap and termination use the fp32 contract (R1, R14),
-// so the per-pixel composited set, T_final and n_contrib match the oracle bit
-// for bit.  The backward replays each pixel's list in reverse, recovers
-// T_k = T_{k+1} / (1 - alpha_k), reduces the 9 per-pair gradients of each entry
-// across the warp with a transposing butterfly (16 shuffles instead of 45)
-// and issues one global atomic per value and warp.
+// consumed in batches of 256: each thread gathers one entry into shared
+// memory (contract record A, B and the fp64 value record; LDS broadcast on
+// use).  A warp stops walking a batch as soon as all its pixels have
+// terminated (vote), the block stops fetching batches once all 256 pixels have
+// (syncthreads_count).
+// Decisions — skip test, alpha cap, termination — use the fp32 contract (R1,
+// R14), so the composited set, T_final and n_contrib match the oracle bit for
+// bit.  The composited VALUES are carried in fp64: the image is
+// the fp64 colour rounded once, and the pixel's full colour
+// C = sum c_k a_k T_k + T_final bg is kept for the single-pass backward (K6).
 #include "contract.cuh"
 #include "internal.cuh"
 
@@ -22,7 +22,10 @@ constexpr int kRasterThreads = kTile * kTile;
 __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* __restrict__ arena, Views v, int view,
                                                               int N, int W, int H, int gx, int ntiles, float bg0,
                                                               float bg1, float bg2, float* __restrict__ image) {
-  __shared__ float4 sA[kRasterThreads], sB[kRasterThreads], sC[kRasterThreads];
+  __shared__ float4 sA[kRasterThreads], sB[kRasterThreads];
+  __shared__ double2 sD[5][kRasterThreads];
+  __shared__ double sExp[64];
+  exp64_table_fill(sExp);
   const int tile = blockIdx.x;
   const int tx = tile % gx, ty = tile / gx;
   const int px = tx * kTile + (threadIdx.x & (kTile - 1));
@@ -36,8 +39,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
   }
   const uint32_t* list = arena + hdr.list_base;
   const float4* rec = v.rec + (size_t)view * N * 3;
+  const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   const float fi = (float)px, fj = (float)py;
-  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+  const double di = px, dj = py;
+  float T = 1.0f;
+  double T64 = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
   uint32_t last = 0, n_exam = 0, n_comp = 0;
   bool done = !inside;
   for (uint32_t b0 = start; b0 < end; b0 += kRasterThreads) {
@@ -47,7 +53,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
       const uint32_t g = list[idx];
       sA[threadIdx.x] = rec[3 * (size_t)g + 0];
       sB[threadIdx.x] = rec[3 * (size_t)g + 1];
-      sC[threadIdx.x] = rec[3 * (size_t)g + 2];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) sD[k][threadIdx.x] = rec64[5 * (size_t)g + k];
     }
     __syncthreads();
     const int n = (int)min((uint32_t)kRasterThreads, end - b0);
@@ -60,17 +67,23 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
       ++n_exam;
       if (power > 0.0f || power < B.y) continue;
       const float ao = mul(B.z, exp_c(power));
-      const float alpha = ao < 0.99f ? ao : 0.99f;
+      const bool capped = !(ao < 0.99f);
+      const float alpha = capped ? 0.99f : ao;
       const float Tn = mul(T, sub(1.0f, alpha));
       if (Tn < 1e-4f) { done = true; continue; }
-      const float4 Cc = sC[j];
-      const float w = alpha * T;
-      C0 = fmaf(Cc.x, w, C0);
-      C1 = fmaf(Cc.y, w, C1);
-      C2 = fmaf(Cc.z, w, C2);
       T = Tn;
       last = b0 + j + 1 - start;
       ++n_comp;
+      // fp64 value of the composited pair
+      const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
+      const double d4x = sD[4][j].x;
+      const double dx = d0.x - di, dy = d0.y - dj;
+      const double a64 = capped ? 0.99 : d2.y * exp64(fma(d1.x * dx, dx, fma(d1.y * dx, dy, d2.x * dy * dy)), sExp);
+      const double w = a64 * T64;
+      C0 = fma(d3.x, w, C0);
+      C1 = fma(d3.y, w, C1);
+      C2 = fma(d4x, w, C2);
+      T64 -= w;   // T64 * (1 - a64)
     }
   }
   {  // pair statistics (one atomic per warp)
@@ -82,14 +95,20 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
   }
   if (inside) {
     const size_t HW = (size_t)W * H, p = (size_t)py * W + px;
-    image[p] = fmaf(T, bg0, C0);
-    image[HW + p] = fmaf(T, bg1, C1);
-    image[2 * HW + p] = fmaf(T, bg2, C2);
+    C0 = fma(T64, (double)bg0, C0);
+    C1 = fma(T64, (double)bg1, C1);
+    C2 = fma(T64, (double)bg2, C2);
+    image[p] = (float)C0;
+    image[HW + p] = (float)C1;
+    image[2 * HW + p] = (float)C2;
+    double* cf = v.cfull + 3 * ((size_t)view * HW + p);
+    cf[0] = C0;
+    cf[1] = C1;
+    cf[2] = C2;
     v.tfinal[(size_t)view * HW + p] = T;
     v.ncontrib[(size_t)view * HW + p] = last;
   }
 }
-
 
 void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* image, int view,
                        const float bg[3], cudaStream_t s) {

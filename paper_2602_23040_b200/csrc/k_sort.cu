@@ -1,20 +1,26 @@
-// K3 — stable LSD radix sort of the visible Gaussians of one view by depth key
+// K3 — onesweep LSD radix sort of the visible Gaussians of one view by depth key
 // (the low "digit" of the (tile, depth) key, row a4), with the culling
 // compaction folded into the first pass.
 //
-// Four 8-bit passes over the 32-bit depth bits.  Each pass: upsweep (per-block
-// digit histogram) -> one-block exclusive scan of the digit-major histogram
-// -> downsweep (stable block-local rank by warp match_any + per-warp digit
-// counters, then scatter).  Input of pass 0 is gid order, so ties in depth
-// keep ascending gid (R8) without carrying the gid in the key.
+//   k_os_hist   one read of every depth key: the four 8-bit digit histograms of
+//               the visible keys (smem histograms, one global atomic per bin and CTA)
+//   k_os_scan   exclusive scan of each histogram -> global digit offsets; n_vis
+//   k_os_pass   x4: each CTA takes a 4096-item tile by atomic ticket, ranks its
+//               items stably per digit (warp match_any + per-warp counters),
+//               publishes its per-digit count, resolves its exclusive prefix by
+//               decoupled look-back over the preceding tiles' status words, and
+//               scatters.  One read and one write of (key, value) per pass.
+// Pass 0 reads the depth keys in gid order and drops culled texels, so ties in
+// depth keep ascending gid (R8) without carrying the gid in the key.
 #include "internal.cuh"
 
 namespace puv {
 
-constexpr int kSortThreads = 256;
-constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 8;                              // per thread
-constexpr int kSortTile = kSortThreads * kSortItems;       // 2048 items per block
+constexpr int kOsThreads = 256;
+constexpr int kOsWarps = kOsThreads / 32;
+constexpr int kOsItems = 16;                         // per thread
+constexpr int kOsTile = kOsThreads * kOsItems;       // 4096 items per CTA
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagPre = 2u << 30, kCountMask = (1u << 30) - 1u;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -22,85 +28,104 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// digit of an item, 256 = "no item" (outside n, or culled in pass 0)
-template <bool FIRST>
-__device__ __forceinline__ uint32_t item_digit(const uint32_t* keys, uint32_t idx, uint32_t n, int shift,
-                                               uint32_t& key) {
-  if (idx >= n) return 256u;
-  key = keys[idx];
-  if (FIRST && key == kInvisible) return 256u;
-  return (key >> shift) & 0xffu;
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-template <bool FIRST>
-__global__ void __launch_bounds__(kSortThreads) k_radix_upsweep(const uint32_t* __restrict__ keys,
-                                                                 const uint32_t* n_ptr, uint32_t n_fixed, int shift,
-                                                                 uint32_t* __restrict__ hist, int nblocks) {
-  __shared__ uint32_t h[256];
-  const uint32_t n = FIRST ? n_fixed : *n_ptr;
-  h[threadIdx.x] = 0;
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kOsThreads) k_os_hist(const uint32_t* __restrict__ keys, uint32_t n,
+                                                       uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += kOsThreads) (&h[0][0])[i] = 0;
   __syncthreads();
-  const uint32_t base = blockIdx.x * kSortTile;
-  if (base < n) {
+  const uint32_t stride = gridDim.x * kOsThreads * 4;
+  for (uint32_t i = (blockIdx.x * kOsThreads + threadIdx.x) * 4; i < n; i += stride) {
+    uint32_t k4[4];
+    if (i + 3 < n && (((uintptr_t)(keys + i)) & 15) == 0) {
+      const uint4 q = *reinterpret_cast<const uint4*>(keys + i);
+      k4[0] = q.x; k4[1] = q.y; k4[2] = q.z; k4[3] = q.w;
+    } else {
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-      uint32_t key;
-      const uint32_t d = item_digit<FIRST>(keys, base + i * kSortThreads + threadIdx.x, n, shift, key);
-      if (d < 256u) atomicAdd(&h[d], 1u);
+      for (int j = 0; j < 4; ++j) k4[j] = i + j < n ? keys[i + j] : kInvisible;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t k = k4[j];
+      if (k == kInvisible) continue;
+      atomicAdd(&h[0][k & 0xffu], 1u);
+      atomicAdd(&h[1][(k >> 8) & 0xffu], 1u);
+      atomicAdd(&h[2][(k >> 16) & 0xffu], 1u);
+      atomicAdd(&h[3][k >> 24], 1u);
     }
   }
   __syncthreads();
-  hist[(size_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+  for (int i = threadIdx.x; i < 4 * 256; i += kOsThreads) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(ghist + i, c);
+  }
 }
 
-// Exclusive scan of `m` u32 in one block of 1024 threads.  If total_out, writes the total.
-__global__ void __launch_bounds__(1024) k_scan_one_block(uint32_t* data, int m, uint32_t* total_out) {
-  __shared__ uint32_t part[1024];
-  const int per = (m + 1023) / 1024;
-  const int lo = threadIdx.x * per, hi = min(m, lo + per);
-  uint32_t s = 0;
-  for (int i = lo; i < hi; ++i) s += data[i];
-  part[threadIdx.x] = s;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    const uint32_t t = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+// ghist[4][256] counts -> exclusive offsets in place; n_vis; reset the pass tickets.
+__global__ void __launch_bounds__(256) k_os_scan(uint32_t* ghist, uint32_t* tickets, uint32_t* n_vis) {
+  __shared__ uint32_t s[256];
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t c = ghist[p * 256 + threadIdx.x];
+    s[threadIdx.x] = c;
     __syncthreads();
-    part[threadIdx.x] += t;
+    for (int off = 1; off < 256; off <<= 1) {
+      const uint32_t t = threadIdx.x >= off ? s[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s[threadIdx.x] += t;
+      __syncthreads();
+    }
+    ghist[p * 256 + threadIdx.x] = s[threadIdx.x] - c;
+    if (p == 0 && threadIdx.x == 255) *n_vis = s[255];
     __syncthreads();
   }
-  uint32_t run = part[threadIdx.x] - s;  // exclusive
-  for (int i = lo; i < hi; ++i) {
-    const uint32_t x = data[i];
-    data[i] = run;
-    run += x;
-  }
-  if (total_out && threadIdx.x == 1023) *total_out = part[1023];
+  if (threadIdx.x < 4) tickets[threadIdx.x] = 0;
 }
 
 template <bool FIRST>
-__global__ void __launch_bounds__(kSortThreads) k_radix_downsweep(const uint32_t* __restrict__ keys_in,
-                                                                   const uint32_t* __restrict__ vals_in,
-                                                                   uint32_t* __restrict__ keys_out,
-                                                                   uint32_t* __restrict__ vals_out,
-                                                                   const uint32_t* n_ptr, uint32_t n_fixed, int shift,
-                                                                   const uint32_t* __restrict__ hist, int nblocks) {
-  __shared__ uint32_t wh[kSortWarps][256];
-  __shared__ uint32_t goff[256];
+__global__ void __launch_bounds__(kOsThreads) k_os_pass(const uint32_t* __restrict__ keys_in,
+                                                       const uint32_t* __restrict__ vals_in,
+                                                       uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                                                       const uint32_t* n_ptr, uint32_t n_fixed, int shift,
+                                                       const uint32_t* __restrict__ goff, uint32_t* status,
+                                                       uint32_t* ticket) {
+  __shared__ uint32_t wh[kOsWarps][256];
+  __shared__ uint32_t excl[256];
+  __shared__ uint32_t s_tile;
   const uint32_t n = FIRST ? n_fixed : *n_ptr;
-  const uint32_t base = blockIdx.x * kSortTile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  for (int i = threadIdx.x; i < kOsWarps * 256; i += kOsThreads) (&wh[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * kOsTile;
   if (base >= n) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&wh[0][0])[i] = 0;
-  goff[threadIdx.x] = hist[(size_t)threadIdx.x * nblocks + blockIdx.x];
-  __syncthreads();
-  uint32_t key[kSortItems], dig[kSortItems], loc[kSortItems], val[kSortItems];
-  const uint32_t wbase = base + warp * (32 * kSortItems);
+  uint32_t key[kOsItems], dig[kOsItems], loc[kOsItems], val[kOsItems];
+  const uint32_t wbase = base + warp * (32 * kOsItems);
 #pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
+  for (int r = 0; r < kOsItems; ++r) {
     const uint32_t idx = wbase + r * 32 + lane;
-    key[r] = 0;
-    dig[r] = item_digit<FIRST>(keys_in, idx, n, shift, key[r]);
-    val[r] = (dig[r] < 256u) ? (FIRST ? idx : vals_in[idx]) : 0u;
+    key[r] = kInvisible;
+    dig[r] = 256u;
+    val[r] = 0u;
+    if (idx < n) {
+      key[r] = keys_in[idx];
+      if (!FIRST || key[r] != kInvisible) {
+        dig[r] = (key[r] >> shift) & 0xffu;
+        val[r] = FIRST ? idx : vals_in[idx];
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
     const uint32_t peers = __match_any_sync(0xffffffffu, dig[r]);
     const uint32_t rank = __popc(peers & lanemask_lt());
     const uint32_t cur = dig[r] < 256u ? wh[warp][dig[r]] : 0u;
@@ -110,24 +135,49 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_downsweep(const uint32_t
     loc[r] = cur + rank;
   }
   __syncthreads();
-  {  // per digit: exclusive prefix over warps
+  // per digit (thread d): exclusive prefix over warps, publish, decoupled look-back
+  {
+    const int d = threadIdx.x;
     uint32_t run = 0;
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) {
-      const uint32_t t = wh[w][threadIdx.x];
-      wh[w][threadIdx.x] = run;
+    for (int w = 0; w < kOsWarps; ++w) {
+      const uint32_t t = wh[w][d];
+      wh[w][d] = run;
       run += t;
+    }
+    uint32_t* st = status + (size_t)tile * 256 + d;
+    if (tile == 0) {
+      st_release(st, kFlagPre | run);
+      excl[d] = 0;
+    } else {
+      st_release(st, kFlagAgg | run);
+      uint32_t acc = 0;
+      for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+        const uint32_t s = ld_volatile(status + (size_t)t * 256 + d);
+        const uint32_t flag = s & ~kCountMask;
+        if (flag == 0u) continue;             // predecessor not published yet: spin
+        acc += s & kCountMask;
+        if (flag == kFlagPre) break;
+        --t;
+      }
+      st_release(st, kFlagPre | (acc + run));
+      excl[d] = acc;
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
+  for (int r = 0; r < kOsItems; ++r) {
     if (dig[r] < 256u) {
-      const uint32_t pos = goff[dig[r]] + wh[warp][dig[r]] + loc[r];
+      const uint32_t pos = goff[dig[r]] + excl[dig[r]] + wh[warp][dig[r]] + loc[r];
       keys_out[pos] = key[r];
       vals_out[pos] = val[r];
     }
   }
+}
+
+size_t depth_sort_scratch_bytes(size_t N) {
+  const size_t tiles = (N + kOsTile - 1) / kOsTile;
+  return 4 * (4 * 256 * tiles + 4 * 256 + 8);
 }
 
 void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cudaStream_t s) {
@@ -136,28 +186,33 @@ void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cud
   uint32_t* sv0 = (uint32_t*)(st + p.sv0);
   uint32_t* sk1 = (uint32_t*)(st + p.sk1);
   uint32_t* sv1 = (uint32_t*)(st + p.sv1);
-  uint32_t* hist = (uint32_t*)(st + p.hist);
-  const int nb = (int)p.sort_blocks;
+  const size_t tiles = ((size_t)p.N + kOsTile - 1) / kOsTile;
+  uint32_t* status = (uint32_t*)(st + p.hist);              // [4][tiles][256]
+  uint32_t* ghist = status + 4 * 256 * tiles;               // [4][256]
+  uint32_t* tickets = ghist + 4 * 256;                      // [4]
   const uint32_t* depth = v.depth + (size_t)view * p.N;
   uint32_t* nvis = &v.hdr[view].n_vis;
   uint32_t* sorted = v.sorted + (size_t)view * p.N;
-  const int m = 256 * nb;
-  // pass 0: depth[] (gid order) -> (sk0, sv0), dropping culled Gaussians; writes n_vis
-  k_radix_upsweep<true><<<nb, kSortThreads, 0, s>>>(depth, nullptr, (uint32_t)p.N, 0, hist, nb);
-  k_scan_one_block<<<1, 1024, 0, s>>>(hist, m, nvis);
-  k_radix_downsweep<true><<<nb, kSortThreads, 0, s>>>(depth, nullptr, sk0, sv0, nullptr, (uint32_t)p.N, 0, hist, nb);
-  const uint32_t* ki[3] = {sk0, sk1, sk0};
-  const uint32_t* vi[3] = {sv0, sv1, sv0};
-  uint32_t* ko[3] = {sk1, sk0, sk1};
-  uint32_t* vo[3] = {sv1, sv0, sorted};
-  for (int pass = 1; pass < 4; ++pass) {
-    const int sh = 8 * pass;
-    k_radix_upsweep<false><<<nb, kSortThreads, 0, s>>>(ki[pass - 1], nvis, 0, sh, hist, nb);
-    k_scan_one_block<<<1, 1024, 0, s>>>(hist, m, nullptr);
-    k_radix_downsweep<false><<<nb, kSortThreads, 0, s>>>(ki[pass - 1], vi[pass - 1], ko[pass - 1], vo[pass - 1], nvis,
-                                                          0, sh, hist, nb);
-  }
-  count_launches(12);
+  cudaMemsetAsync(status, 0, 4 * (4 * 256 * tiles + 4 * 256), s);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t hwant = ((size_t)p.N + 4 * kOsThreads - 1) / (4 * kOsThreads);
+  const int hb = (int)(hwant < (size_t)4 * nsm ? (hwant > 0 ? hwant : 1) : (size_t)4 * nsm);
+  k_os_hist<<<hb, kOsThreads, 0, s>>>(depth, (uint32_t)p.N, ghist);
+  k_os_scan<<<1, 256, 0, s>>>(ghist, tickets, nvis);
+  const uint32_t* ki[4] = {depth, sk0, sk1, sk0};
+  const uint32_t* vi[4] = {nullptr, sv0, sv1, sv0};
+  uint32_t* ko[4] = {sk0, sk1, sk0, sk1};
+  uint32_t* vo[4] = {sv0, sv1, sv0, sorted};
+  const int grid = (int)tiles;
+  k_os_pass<true><<<grid, kOsThreads, 0, s>>>(ki[0], vi[0], ko[0], vo[0], nullptr, (uint32_t)p.N, 0, ghist, status,
+                                              tickets);
+  for (int pass = 1; pass < 4; ++pass)
+    k_os_pass<false><<<grid, kOsThreads, 0, s>>>(ki[pass], vi[pass], ko[pass], vo[pass], nvis, 0, 8 * pass,
+                                                 ghist + 256 * pass, status + (size_t)pass * 256 * tiles,
+                                                 tickets + pass);
+  count_launches(6);
 }
 
 }  // namespace puv

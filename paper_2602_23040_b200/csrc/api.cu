@@ -114,7 +114,7 @@ static puv_status check_cameras(int n, const puv_camera* cams, int& W, int& H) {
       return fail(PUV_E_INVALID_CAMERA, "camera %d: fx, fy, near must be > 0 and the image non-empty", i);
     if (c.width != W || c.height != H)
       return fail(PUV_E_DIMENSION_MISMATCH, "camera %d: %dx%d differs from camera 0 (%dx%d)", i, c.width, c.height, W, H);
-    if ((int64_t)W * H >= (int64_t)1 << 30 || (W + kTile - 1) / kTile > 65535 || (H + kTile - 1) / kTile > 65535)
+    if ((int64_t)W * H >= (int64_t)1 << 30 || (W + kTile - 1) / kTile > 2048 || (H + kTile - 1) / kTile > 65535)
       return fail(PUV_E_UNSUPPORTED, "camera %d: image %dx%d too large", i, W, H);
     for (int a = 0; a < 3; ++a)
       for (int b = 0; b < 3; ++b) {
@@ -177,6 +177,7 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.koff = take(4 * (N + 1));
   p.bsum = take(4 * (N / 2048 + 2));
   p.cnt = take(4 * (size_t)kNbMax * p.ntiles);
+  p.bstart = take(4 * (size_t)(kNbMax + 1));
   p.total = off;
   return p;
 }

@@ -57,7 +57,7 @@ struct Plan {
   // per view arrays, each [n_views][...]
   size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull;
   // scratch shared by all views (reused in stream order)
-  size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt;
+  size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt, bstart;
   size_t sort_blocks;      // blocks of one radix pass over N items
   size_t total;
 };

@@ -28,8 +28,10 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
   exp64_table_fill(sExp);
   const int tile = blockIdx.x;
   const int tx = tile % gx, ty = tile / gx;
-  const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int py = ty * kTile + (threadIdx.x / kTile);
+  // compact 8x4 warp footprint: warp w covers columns 8(w&1).. and rows 4(w>>1)..
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
   const bool inside = px < W && py < H;
   const ViewHdr& hdr = v.hdr[view];
   uint32_t start = 0, end = 0;

@@ -1,18 +1,21 @@
 // K6 k_raster_bwd — per-tile gradient of the front-to-back composite (row a7).
 //
-// One 128-thread block per 16x16 tile; each thread owns PPT = 2 pixels of a
-// column (rows r, r+8).  Every decision (skip test R1, alpha cap, composited
-// set R14) is replayed with the fp32 contract exactly as K5 took it; every
-// VALUE is fp64 (fp32 values cannot hold 1e-3 relative per
-// component on cancellation-heavy gradient components).  Single pass in
-// front-to-back order, using the pixel's full colour C from K5:
+// One 128-thread block (4 warps) per 16x16 tile; warp w owns the 8x8 pixel
+// quadrant (8(w&1), 8(w>>1)); lane l owns column l & 7 and rows (l >> 3) + 4k,
+// k < PPT = 2.  Every decision (skip test R1, alpha cap, composited set R14) is
+// replayed with the fp32 contract exactly as K5 took it; every VALUE is fp64
+// (DESIGN.md §5).  Single pass in front-to-back order, using the pixel's full
+// colour C from K5:
 //   T_k = prod_{i<k} (1 - a_i),   P_k = sum_{i<=k} c_i a_i T_i,   S_k = C - P_k
 //   dL/dc_k = a_k T_k dL/dC
 //   dL/da_k = sum_ch dL/dC (T_k c_k - S_k / (1 - a_k))
 //   uncapped: dL/do = G dL/da, dL/dpower = o G dL/da -> (mx, my, ha, nb, hc)
-// A thread sums the 9 values of an entry over its pixels, the warp sums them
-// with a transposing butterfly (16 double shuffles instead of 45) and 9 lanes
-// issue one fp64 atomic each into the (view, Gaussian) gradient slot.
+// The per-pixel body is branch-free (inactive pixels get a = 0 and masked
+// terms), so the pixels' fp64 chains interleave (ncu: the branchy version was
+// bound by fixed-latency "wait" stalls).  A thread sums the 9 values of an
+// entry over its pixels; the warp sums them with a transposing butterfly
+// (8 values in 9 double shuffles, the 9th in 5) and 9 lanes issue one fp64
+// atomic each into the (view, Gaussian) gradient slot.
 #include "contract.cuh"
 #include "internal.cuh"
 
@@ -21,14 +24,13 @@ namespace puv {
 constexpr int kBwdPPT = 2;                                 // pixels per thread
 constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128
 constexpr int kBwdBatch = 128;                             // entries staged per batch
-constexpr int kBwdRowStep = kTile / kBwdPPT;                // 8
 
-// Sum 16 values across the warp; afterwards lane l holds the total of value (l >> 1).
-__device__ __forceinline__ double butterfly16(double (&x)[16]) {
+// Sum v[0..7] across the warp (lane l ends with the total of value (l >> 2) & 7) and v8 (all lanes).
+__device__ __forceinline__ double warp_reduce9(double (&x)[8], double& v8) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int level = 0; level < 4; ++level) {
-    const int half = 8 >> level;
+  for (int level = 0; level < 3; ++level) {
+    const int half = 4 >> level;
     const int off = 16 >> level;
     const bool upper = (lane & off) != 0;
 #pragma unroll
@@ -38,7 +40,20 @@ __device__ __forceinline__ double butterfly16(double (&x)[16]) {
       x[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
   }
-  return x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
+  double s = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, off);
+  return s;
+}
+
+// 1/y for y in [0.01, 1]: fp32 reciprocal estimate + two Newton steps in fp64 (~1 ulp)
+__device__ __forceinline__ double rcp64(double y) {
+  double r = (double)__frcp_rn((float)y);
+  double e = fma(-y, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-y, r, 1.0);
+  return fma(r, e, r);
 }
 
 __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int view,
@@ -61,22 +76,23 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   double* g2 = v.grad2d + (size_t)view * N * 9;
   const size_t HW = (size_t)W * H;
-  const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int py0 = ty * kTile + (threadIdx.x / kTile);
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int py0 = ty * kTile + (warp >> 1) * 8 + (lane >> 3);
   const float fi = (float)px;
   const double di = px;
   float fj[kBwdPPT];
   uint32_t last[kBwdPPT];
-  double dC[kBwdPPT][3], S[kBwdPPT][3], T[kBwdPPT];
+  float dC[kBwdPPT][3];
+  double S[kBwdPPT][3], T[kBwdPPT];
   uint32_t tlast = 0;
 #pragma unroll
   for (int k = 0; k < kBwdPPT; ++k) {
-    const int py = py0 + kBwdRowStep * k;
+    const int py = py0 + 4 * k;
     fj[k] = (float)py;
     last[k] = 0;
     T[k] = 1.0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) dC[k][c] = S[k][c] = 0.0;
+    for (int c = 0; c < 3; ++c) { dC[k][c] = 0.f; S[k][c] = 0.0; }
     if (px < W && py < H) {
       const size_t p = (size_t)py * W + px;
       last[k] = v.ncontrib[(size_t)view * HW + p];
@@ -111,52 +127,53 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
     for (int j = 0; j < n; ++j) {
       const uint32_t e = lo + j;
       if (e >= wlast) break;  // warp-uniform: no pixel of this warp reaches entry e
-      double gv[16];
+      const float4 A = sA[j], B = sB[j];
+      // decisions (fp32 contract), per pixel
+      bool act[kBwdPPT], cap[kBwdPPT];
+      bool any = false;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) gv[k] = 0.0;
-      bool act = false;
-      if (e < tlast) {
-        const float4 A = sA[j], B = sB[j];
-        const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
-        const double d4x = sD[4][j].x;
+      for (int k = 0; k < kBwdPPT; ++k) {
+        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi, fj[k]);
+        act[k] = e < last[k] && !(power > 0.0f || power < B.y);
+        cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
+        any |= act[k];
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
+      const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
+      const double d4x = sD[4][j].x;
+      double gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      double gb = 0.0;
 #pragma unroll
-        for (int k = 0; k < kBwdPPT; ++k) {
-          if (e >= last[k]) continue;
-          const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi, fj[k]);
-          if (power > 0.0f || power < B.y) continue;
-          const bool capped = !(mul(B.z, exp_c(power)) < 0.99f);
-          act = true;
-          const double dx = d0.x - di, dy = d0.y - (double)fj[k];
-          const double G = exp64(fma(d1.x * dx, dx, fma(d1.y * dx, dy, d2.x * dy * dy)), sExp);
-          const double a = capped ? 0.99 : d2.y * G;
-          const double aT = a * T[k];
-          S[k][0] = fma(-d3.x, aT, S[k][0]);
-          S[k][1] = fma(-d3.y, aT, S[k][1]);
-          S[k][2] = fma(-d4x, aT, S[k][2]);
-          const double iom = 1.0 / (1.0 - a);
-          const double dLda = dC[k][0] * (T[k] * d3.x - S[k][0] * iom) + dC[k][1] * (T[k] * d3.y - S[k][1] * iom) +
-                              dC[k][2] * (T[k] * d4x - S[k][2] * iom);
-          gv[6] = fma(aT, dC[k][0], gv[6]);
-          gv[7] = fma(aT, dC[k][1], gv[7]);
-          gv[8] = fma(aT, dC[k][2], gv[8]);
-          if (!capped) {
-            const double GdL = G * dLda;
-            const double dP = d2.y * GdL;                    // d alpha / d power = o G
-            gv[5] += GdL;                                    // d alpha / d o = G
-            gv[2] = fma(dx * dx, dP, gv[2]);
-            gv[3] = fma(dx * dy, dP, gv[3]);
-            gv[4] = fma(dy * dy, dP, gv[4]);
-            gv[0] = fma(2.0 * d1.x * dx + d1.y * dy, dP, gv[0]);
-            gv[1] = fma(d1.y * dx + 2.0 * d2.x * dy, dP, gv[1]);
-          }
-          T[k] -= aT;                                        // T_{k+1} = T_k (1 - a_k)
-        }
+      for (int k = 0; k < kBwdPPT; ++k) {
+        const double dx = d0.x - di, dy = d0.y - (double)fj[k];
+        const double pw = fmax(fma(d1.x * dx, dx, fma(d1.y * dx, dy, d2.x * dy * dy)), -700.0);
+        const double G = exp64(fmin(pw, 0.0), sExp);
+        const double a = act[k] ? (cap[k] ? 0.99 : d2.y * G) : 0.0;
+        const double aT = a * T[k];
+        S[k][0] = fma(-d3.x, aT, S[k][0]);
+        S[k][1] = fma(-d3.y, aT, S[k][1]);
+        S[k][2] = fma(-d4x, aT, S[k][2]);
+        const double iom = rcp64(1.0 - a);
+        const double c0 = dC[k][0], c1 = dC[k][1], c2 = dC[k][2];
+        const double dLda = c0 * (T[k] * d3.x - S[k][0] * iom) + c1 * (T[k] * d3.y - S[k][1] * iom) +
+                            c2 * (T[k] * d4x - S[k][2] * iom);
+        gv[6] = fma(aT, c0, gv[6]);
+        gv[7] = fma(aT, c1, gv[7]);
+        gb = fma(aT, c2, gb);
+        const double GdL = (act[k] && !cap[k]) ? G * dLda : 0.0;
+        const double dP = d2.y * GdL;                        // d alpha / d power = o G
+        gv[5] += GdL;                                        // d alpha / d o = G
+        gv[2] = fma(dx * dx, dP, gv[2]);
+        gv[3] = fma(dx * dy, dP, gv[3]);
+        gv[4] = fma(dy * dy, dP, gv[4]);
+        gv[0] = fma(2.0 * d1.x * dx + d1.y * dy, dP, gv[0]);
+        gv[1] = fma(d1.y * dx + 2.0 * d2.x * dy, dP, gv[1]);
+        T[k] -= aT;                                          // T_{k+1} = T_k (1 - a_k)
       }
-      if (__any_sync(0xffffffffu, act)) {
-        const double s = butterfly16(gv);
-        const int vi = lane >> 1;
-        if ((lane & 1) == 0 && vi < 9) atomicAdd(g2 + 9 * (size_t)sG[j] + vi, s);
-      }
+      const double s = warp_reduce9(gv, gb);
+      double* dst = g2 + 9 * (size_t)sG[j];
+      if ((lane & 3) == 0) atomicAdd(dst + (lane >> 2), s);
+      if (lane == 1) atomicAdd(dst + 8, gb);
     }
   }
 }

@@ -170,10 +170,10 @@ def stage_work(stage, c, D):
         return "hbm", 4 * N + 4 * nv
     if stage == "bin":              # read rank rects, write every key once, ranges
         return "hbm", 8 * nv + 4 * K + 8 * c["ntiles"]
-    if stage == "raster_fwd":       # fp32 lane-ops: 9 per examined pair, +21 per composited pair
-        return "alu_fp32", 9 * E + 21 * P
-    if stage == "raster_bwd":       # fp64 lane-ops per composited pair (2 exp64 + chain) ~ 90
-        return "alu_fp64", 90 * P
+    if stage == "raster_fwd":       # fp64 lane-ops of the value path: 24 per composited pair
+        return "alu_fp64", 24 * P
+    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 58
+        return "alu_fp64", 58 * P
     if stage == "project_bwd":      # read 2D grads + params, RMW texel grads
         return "hbm", 72 * nv + (D * 4 * 3 * N) / c["views"]
     if stage == "loss":
@@ -326,6 +326,13 @@ def main():
                 "peak_source": f"derived: {nsm} SMs x {lanes} {kind[4:]} lanes x {sm_mhz:.0f} MHz (DESIGN.md §6)"}
     roof["kernel"] = dom
     roof["avg_launch_ms"] = avg_launch_s * 1000.0
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp) and args.config == 3:
+        tj = json.load(open(tp))
+        if dom in tj.get("bytes_per_launch", {}):
+            # ncu capture of the same kernel on C3, scaled to this run's views per launch
+            roof["traffic"] = tj["bytes_per_launch"][dom] / tj["views_per_launch"][dom] * (units / calls)
+            roof["traffic_unit"] = "bytes/launch (ncu dram read+write)"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -60,6 +60,37 @@ struct StageScope {
   }
 };
 
+// ---- internal streams for the binning pipeline (one set per device, created on first use) ----
+struct StreamSet {
+  cudaStream_t s[kBinStreams] = {};
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t view_event(int v) {
+    while ((int)ev.size() <= v) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      ev.push_back(e);
+    }
+    return ev[v];
+  }
+};
+
+static StreamSet& stream_set(int /*n*/) {
+  static std::mutex mu;
+  static std::vector<StreamSet*> sets;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)sets.size() <= dev) sets.resize(dev + 1, nullptr);
+  if (!sets[dev]) {
+    StreamSet* ss = new StreamSet();
+    for (int i = 0; i < kBinStreams; ++i) cudaStreamCreateWithFlags(&ss->s[i], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ss->fork, cudaEventDisableTiming);
+    sets[dev] = ss;
+  }
+  return *sets[dev];
+}
+
 static puv_status fail(puv_status code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -169,15 +200,21 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.ncontrib = take(4 * V * p.HW);
   p.cfull = take(24 * V * p.HW);
   p.sort_blocks = (N + 2047) / 2048;
-  p.sk0 = take(4 * N);
-  p.sv0 = take(4 * N);
-  p.sk1 = take(4 * N);
-  p.sv1 = take(4 * N);
-  p.hist = take(depth_sort_scratch_bytes(N));
-  p.koff = take(4 * (N + 1));
-  p.bsum = take(4 * (N / 2048 + 2));
-  p.cnt = take(4 * (size_t)kNbMax * p.ntiles);
-  p.bstart = take(4 * (size_t)(kNbMax + 1));
+  // binning scratch: one block per binning stream; offsets below are relative to a block
+  size_t soff = 0;
+  auto stake = [&](size_t bytes) { const size_t o = soff; soff += align_up(bytes); return o; };
+  p.sk0 = stake(4 * N);
+  p.sv0 = stake(4 * N);
+  p.sk1 = stake(4 * N);
+  p.sv1 = stake(4 * N);
+  p.hist = stake(depth_sort_scratch_bytes(N));
+  p.koff = stake(4 * (N + 1));
+  p.bsum = stake(4 * (N / 2048 + 2));
+  p.cnt = stake(4 * (size_t)kNbMax * p.ntiles);
+  p.bstart = stake(4 * (size_t)(kNbMax + 1));
+  p.nscratch = n_views < kBinStreams ? n_views : kBinStreams;
+  p.scratch_stride = soff;
+  p.scratch0 = take(soff * p.nscratch);
   p.total = off;
   return p;
 }
@@ -325,9 +362,20 @@ puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_
     StageScope sc(PUV_STAGE_PROJECT, s);
     launch_project(p, c.views, c.P, atlas_occ, cb, s);
   }
+  // Pipeline: view v is depth-sorted and binned on binning stream v % nscratch (its own scratch
+  // block) while earlier views composite on `s`; `s` waits on view v's binning event only.
+  StreamSet& ss = stream_set(p.nscratch);
+  cudaEventRecord(ss.fork, s);
+  for (int i = 0; i < p.nscratch; ++i) cudaStreamWaitEvent(ss.s[i], ss.fork, 0);
   for (int v = 0; v < n_views; ++v) {
-    { StageScope sc(PUV_STAGE_DEPTH_SORT, s); launch_depth_sort(p, c.views, state, v, s); }
-    { StageScope sc(PUV_STAGE_BIN, s); launch_bin(p, c.views, state, (uint32_t*)arena, v, s); }
+    const int i = v % p.nscratch;
+    cudaStream_t bs = ss.s[i];
+    void* scratch = (char*)state + p.scratch0 + (size_t)i * p.scratch_stride;
+    { StageScope sc(PUV_STAGE_DEPTH_SORT, bs); launch_depth_sort(p, c.views, scratch, v, bs); }
+    { StageScope sc(PUV_STAGE_BIN, bs); launch_bin(p, c.views, scratch, (uint32_t*)arena, v, bs); }
+    cudaEvent_t done = ss.view_event(v);
+    cudaEventRecord(done, bs);
+    cudaStreamWaitEvent(s, done, 0);
     { StageScope sc(PUV_STAGE_RASTER_FWD, s);
       launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)v * 3 * p.HW, v, bg, s); }
   }

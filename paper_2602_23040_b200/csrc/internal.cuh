@@ -12,6 +12,7 @@ constexpr int kMaxPlanes = 11 + 3 * 16;   // SH degree 3
 constexpr int kCamBatch = 64;             // views per K1/K7 launch (cameras passed by value, 6 KB of params)
 constexpr int kTile = PUV_TILE;
 constexpr int kNbMax = 1024;              // max key blocks of the stable tile pass per view
+constexpr int kBinStreams = 4;            // views binned concurrently (one scratch block each)
 constexpr uint32_t kInvisible = 0xFFFFFFFFu;
 
 struct PlaneTab { const float* p[kMaxPlanes]; };
@@ -57,7 +58,10 @@ struct Plan {
   // per view arrays, each [n_views][...]
   size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull;
   // scratch shared by all views (reused in stream order)
+  // (offsets relative to one scratch block; block i starts at scratch0 + i * scratch_stride)
   size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt, bstart;
+  size_t scratch0, scratch_stride;
+  int nscratch;            // binning streams / scratch blocks of this call
   size_t sort_blocks;      // blocks of one radix pass over N items
   size_t total;
 };

@@ -136,14 +136,17 @@ __global__ void __launch_bounds__(kScanThreads) k_koff_write(const uint32_t* __r
   }
 }
 
+// Views are binned concurrently on several streams: the arena is carved with atomics (a view's
+// list_base depends on the completion order; its contents do not).
 __global__ void k_view_finalize(ViewHdr* hdr, CallHdr* call, const uint64_t* ktotal) {
   const uint64_t K = *ktotal;
   hdr->K = K;
-  call->arena_need += K;
-  const bool fits = K < 0xffffffffull && call->arena_used + K <= call->arena_cap;
+  atomicAdd((unsigned long long*)&call->arena_need, (unsigned long long)K);
+  const uint64_t base = K < 0xffffffffull ? atomicAdd((unsigned long long*)&call->arena_used, (unsigned long long)K)
+                                          : ~0ull;
+  const bool fits = base != ~0ull && base + K <= call->arena_cap;
   if (fits) {
-    hdr->list_base = call->arena_used;
-    call->arena_used += K;
+    hdr->list_base = base;
     hdr->overflow = 0;
     uint64_t kb = (K + kNbMax - 1) / kNbMax;
     if (kb < 65536) kb = 65536;

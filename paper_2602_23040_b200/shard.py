@@ -20,6 +20,13 @@ def local_views(n_views: int, rank: int, world: int) -> list[int]:
     return [v for v in range(n_views) if v % world == rank]
 
 
+def reduce_gradients(grad: torch.Tensor, loss: torch.Tensor, world: int, group=None) -> None:
+    """The one exchange of the path (row a10): sum the atlas gradient planes and the loss over ranks."""
+    if world > 1:
+        dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
+
+
 class ShardedStep:
     """One fwd + loss + bwd step over this rank's views, then the gradient all-reduce."""
 
@@ -46,9 +53,7 @@ class ShardedStep:
                              self.R.arena)
         puv.l2_loss_grad(self.images, targets, self.dL, self.loss)
         self.R.backward(atlas, occ, self.dL, grad=grad, mask=mask)
-        if self.world > 1:
-            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
-            dist.all_reduce(self.loss, op=dist.ReduceOp.SUM, group=self.group)
+        reduce_gradients(grad, self.loss, self.world, self.group)
         return self.loss
 
     def overflowed(self) -> bool:

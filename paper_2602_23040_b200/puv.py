@@ -133,10 +133,15 @@ def _ptr_table(tensors):
     return (C.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
 
 
-def _planes(t: torch.Tensor):
-    """(D, H, W) fp32 CUDA tensor -> host table of D plane pointers."""
-    assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous(), "planes: contiguous fp32 CUDA (D,H,W)"
-    return _ptr_table([t[d] for d in range(t.shape[0])])
+def _planes(t):
+    """(D, H, W) fp32 CUDA tensor, or a sequence of D contiguous (H, W) fp32 CUDA tensors (planes may be
+    shared between atlases, e.g. the constant planes of a frame sequence) -> host table of D pointers."""
+    if isinstance(t, torch.Tensor):
+        assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous(), "planes: contiguous fp32 CUDA (D,H,W)"
+        return _ptr_table([t[d] for d in range(t.shape[0])])
+    for p in t:
+        assert p.is_cuda and p.dtype == torch.float32 and p.is_contiguous(), "planes: contiguous fp32 CUDA (H,W)"
+    return _ptr_table(list(t))
 
 
 def camera(viewmat, fx, fy, cx, cy, width, height, near, campos) -> Camera:
@@ -320,7 +325,8 @@ class Renderer:
 
     def backward(self, atlas, occ, dL, grad=None, mask=None, stream=None):
         if grad is None:
-            grad = torch.zeros_like(atlas)
+            grad = (torch.zeros_like(atlas) if isinstance(atlas, torch.Tensor) else
+                    torch.zeros((len(atlas),) + tuple(atlas[0].shape), dtype=torch.float32, device=self.device))
         render_backward(self.layout, atlas, occ, self.cams, self.opts, dL, mask, self.state, self.arena, grad,
                         stream)
         return grad

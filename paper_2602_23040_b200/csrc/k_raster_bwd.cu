@@ -76,18 +76,17 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   double* g2 = v.grad2d + (size_t)view * N * 9;
   const size_t HW = (size_t)W * H;
-  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-  const int py0 = ty * kTile + (warp >> 1) * 8 + (lane >> 3);
-  const float fi = (float)px;
-  const double di = px;
-  float fj[kBwdPPT];
+  float fi[kBwdPPT], fj[kBwdPPT];
   uint32_t last[kBwdPPT];
   float dC[kBwdPPT][3];
   double S[kBwdPPT][3], T[kBwdPPT];
   uint32_t tlast = 0;
 #pragma unroll
   for (int k = 0; k < kBwdPPT; ++k) {
-    const int py = py0 + 4 * k;
+    // compact 8x8 warp footprint: warp w owns quadrant (8(w&1), 8(w>>1)), lane l column l&7, rows (l>>3)+4k
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (warp >> 1) * 8 + (lane >> 3) + 4 * k;
+    fi[k] = (float)px;
     fj[k] = (float)py;
     last[k] = 0;
     T[k] = 1.0;
@@ -133,7 +132,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
       bool any = false;
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi, fj[k]);
+        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
         act[k] = e < last[k] && !(power > 0.0f || power < B.y);
         cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
         any |= act[k];
@@ -145,7 +144,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
       double gb = 0.0;
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const double dx = d0.x - di, dy = d0.y - (double)fj[k];
+        const double dx = d0.x - (double)fi[k], dy = d0.y - (double)fj[k];
         const double pw = fmax(fma(d1.x * dx, dx, fma(d1.y * dx, dy, d2.x * dy * dy)), -700.0);
         const double G = exp64(fmin(pw, 0.0), sExp);
         const double a = act[k] ? (cap[k] ? 0.99 : d2.y * G) : 0.0;

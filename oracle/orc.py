@@ -68,6 +68,7 @@ def lib():
         L.orc_forward.argtypes = [P, P, C.c_int, C.c_int64, P, P, P, P, P, P, P]
         L.orc_backward.argtypes = [P, P, C.c_int, C.c_int64, P, P, P, P, P, P]
         L.orc_layout_column.argtypes = [C.c_int, P, P, P, P, P]
+        L.orc_label_dynamic.argtypes = [P, C.c_int64, P, C.c_int, P, P, C.c_int, P, C.c_int64, P]
         L.orc_pack.argtypes = [C.c_int, P, P, P, C.c_int, P, P, C.c_int32, C.c_int32, P, P]
         _LIB = L
     return _LIB
@@ -241,6 +242,28 @@ def backward(planes, occ, sh_degree, cam, dL_dimage, mask=None, bg=(0.0, 0.0, 0.
                             _ptr(bgv), _ptr(dl), mask_p, _ptr_table(gl))
     assert rc == 0
     return grad
+
+
+def label_dynamic(planes, occ, cams, masks, r_max=64, gids=None):
+    """Supp. Alg. 1: D_i = OR_c [exists pixel p, |p-m|_inf <= r, d^2 <= 9, M_c(p)].
+    masks: (n_cams, H, W) uint8.  gids: optional texel ids to label (others returned as 0)."""
+    D, HA, WA = planes.shape
+    n = HA * WA
+    pl = [np.ascontiguousarray(planes[d].reshape(-1)) for d in range(D)]
+    arr = (OrcCamera * len(cams))(*[camera(c) for c in cams])
+    m = np.ascontiguousarray(masks, np.uint8)
+    assert m.shape == (len(cams), cams[0].height, cams[0].width)
+    labels = np.zeros(n, np.uint8)
+    occ_p = _ptr(np.ascontiguousarray(occ.reshape(-1))) if occ is not None else None
+    if gids is not None:
+        g = np.ascontiguousarray(gids, np.int64)
+        rc = lib().orc_label_dynamic(_ptr_table(pl), n, occ_p, len(cams), arr, _ptr(m), r_max, _ptr(g), g.size,
+                                     _ptr(labels))
+    else:
+        rc = lib().orc_label_dynamic(_ptr_table(pl), n, occ_p, len(cams), arr, _ptr(m), r_max, None, 0,
+                                     _ptr(labels))
+    assert rc == 0
+    return labels.reshape(HA, WA)
 
 
 def l2_loss_grad(image, target):

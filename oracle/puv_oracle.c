@@ -721,6 +721,101 @@ int orc_backward(const float* const* dec, const double* const* val, int sh_degre
 }
 
 /* ------------------------------------------------------------------------- */
+/* covariance-aware flow masking, supp. Algorithm 1,
+ * followed step by step with the readings M1-M6 of DESIGN.md §10:
+ *   1. Sigma3D = R(q) diag(s^2) R(q)^T            (contract U1-U4)
+ *   2. camera-space mean; J = [[fx/z,0,-fx x/z^2],[0,fy/z,-fy y/z^2]] UNclamped;
+ *      Sigma2D = J (T Sigma T^T) J^T; +0.3 on the diagonal; m = pixel projection
+ *   3. invalid (static for this camera) if det <= 1e-7, det < 0 or z <= 0
+ *   4. r = min(r_max, ceil(3 sqrt(lambda_max)))
+ *   5. scan integer pixels p with |p - m|_inf <= r inside the image; dynamic iff
+ *      some p has d^2 <= 9 (contract: R1 power >= -4.5) and mask(p) = 1
+ *   D_i = OR over cameras.  labels: n bytes, OVERWRITTEN.  masks: n_cams images
+ *   of width*height bytes (0 / nonzero), camera order.                        */
+
+static int label_one_f32(const float* const* planes, int64_t g, const orc_camera* cam, const uint8_t* mask,
+                         int r_max)
+{
+    float s0 = orc_exp_c(planes[3][g]), s1 = orc_exp_c(planes[4][g]), s2 = orc_exp_c(planes[5][g]);
+    float t0 = s0 * s0, t1 = s1 * s1, t2 = s2 * s2;
+    float w = planes[6][g], x = planes[7][g], y = planes[8][g], z = planes[9][g];
+    float n2 = ((w * w + x * x) + y * y) + z * z;
+    if (n2 == 0.0f) return 0;
+    float n = sqrtf(n2);
+    w = w / n; x = x / n; y = y / n; z = z / n;
+    float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
+    float wx = w * x, wy = w * y, wz = w * z;
+    float R[3][3];
+    R[0][0] = 1.0f - 2.0f * (yy + zz); R[0][1] = 2.0f * (xy - wz);        R[0][2] = 2.0f * (xz + wy);
+    R[1][0] = 2.0f * (xy + wz);        R[1][1] = 1.0f - 2.0f * (xx + zz); R[1][2] = 2.0f * (yz - wx);
+    R[2][0] = 2.0f * (xz - wy);        R[2][1] = 2.0f * (yz + wx);        R[2][2] = 1.0f - 2.0f * (xx + yy);
+    float S[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = a; b < 3; ++b) {
+            float v = ((R[a][0] * t0) * R[b][0] + (R[a][1] * t1) * R[b][1]) + (R[a][2] * t2) * R[b][2];
+            S[a][b] = v; S[b][a] = v;
+        }
+    const float* V = cam->viewmat;
+    float mux = planes[0][g], muy = planes[1][g], muz = planes[2][g];
+    float px = ((V[0] * mux + V[1] * muy) + V[2] * muz) + V[3];
+    float py = ((V[4] * mux + V[5] * muy) + V[6] * muz) + V[7];
+    float pz = ((V[8] * mux + V[9] * muy) + V[10] * muz) + V[11];
+    if (!(pz > 0.0f)) return 0;
+    float ux = px / pz, uy = py / pz;
+    float J00 = cam->fx / pz, J02 = -((cam->fx * ux) / pz);
+    float J11 = cam->fy / pz, J12 = -((cam->fy * uy) / pz);
+    float T[2][3];
+    for (int k = 0; k < 3; ++k) {
+        T[0][k] = J00 * V[0 * 4 + k] + J02 * V[2 * 4 + k];
+        T[1][k] = J11 * V[1 * 4 + k] + J12 * V[2 * 4 + k];
+    }
+    float Wm[2][3];
+    for (int a = 0; a < 2; ++a)
+        for (int i = 0; i < 3; ++i)
+            Wm[a][i] = (S[i][0] * T[a][0] + S[i][1] * T[a][1]) + S[i][2] * T[a][2];
+    float ca = (T[0][0] * Wm[0][0] + T[0][1] * Wm[0][1]) + T[0][2] * Wm[0][2];
+    float cb = (T[1][0] * Wm[0][0] + T[1][1] * Wm[0][1]) + T[1][2] * Wm[0][2];
+    float cc = (T[1][0] * Wm[1][0] + T[1][1] * Wm[1][1]) + T[1][2] * Wm[1][2];
+    ca = ca + 0.3f; cc = cc + 0.3f;
+    float det = ca * cc - cb * cb;
+    if (!(det > 1e-7f)) return 0;
+    float ha = -0.5f * (cc / det), nb = cb / det, hc = -0.5f * (ca / det);
+    float tr = ca + cc;
+    float lam = 0.5f * (tr + sqrtf(fmaxf(0.0f, tr * tr - 4.0f * det)));
+    float rf = fminf((float)r_max, ceilf(3.0f * sqrtf(lam)));
+    float mx = cam->fx * ux + cam->cx, my = cam->fy * uy + cam->cy;
+    float fx0 = fmaxf(ceilf(mx - rf), 0.0f), fx1 = fminf(floorf(mx + rf), (float)(cam->width - 1));
+    float fy0 = fmaxf(ceilf(my - rf), 0.0f), fy1 = fminf(floorf(my + rf), (float)(cam->height - 1));
+    if (fx0 > fx1 || fy0 > fy1) return 0;
+    for (int j = (int)fy0; j <= (int)fy1; ++j)
+        for (int i = (int)fx0; i <= (int)fx1; ++i) {
+            if (!mask[(int64_t)j * cam->width + i]) continue;
+            float dx = mx - (float)i, dy = my - (float)j;
+            float u = fmaf(nb, dy, ha * dx);
+            float power = fmaf(dx, u, (hc * dy) * dy);
+            if (power >= -4.5f) return 1;
+        }
+    return 0;
+}
+
+/* gids: nullable list of n_sel texel ids to label (others untouched); NULL = all n texels */
+int orc_label_dynamic(const float* const* planes, int64_t n, const uint8_t* occ, int n_cams, const orc_camera* cams,
+                      const uint8_t* masks, int r_max, const int64_t* gids, int64_t n_sel, uint8_t* labels)
+{
+    int64_t cnt = gids ? n_sel : n;
+    for (int64_t s = 0; s < cnt; ++s) {
+        int64_t g = gids ? gids[s] : s;
+        uint8_t d = 0;
+        if (!occ || occ[g])
+            for (int c = 0; c < n_cams && !d; ++c)
+                d = (uint8_t)label_one_f32(planes, g, &cams[c],
+                                            masks + (int64_t)c * cams[0].width * cams[0].height, r_max);
+        labels[g] = d;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
 /* atlas layout and packing (R15)                 */
 
 /* Column layout for arbitrary level lists: L0 at (0,0); levels 1.. stacked

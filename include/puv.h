@@ -140,6 +140,20 @@ puv_status puv_render_backward(const puv_layout* layout, const float* const* atl
                                const float* dL_dimages, const uint8_t* dynamic_mask, void* state, size_t state_bytes,
                                void* arena, size_t arena_bytes, float* const* atlas_grad, void* stream);
 
+/* Covariance-aware flow masking, supp. Algorithm 1: the dynamic label
+ *   D_i = OR_c [ exists integer pixel p inside the image with |p - m_ic|_inf <= r_ic,
+ *                mask_c(p) != 0 and (p - m_ic)^T (Sigma2D_ic)^-1 (p - m_ic) <= 9 ],
+ *   r_ic = min(r_max, ceil(3 sqrt(lambda_max))), Sigma2D with the UNclamped EWA Jacobian + 0.3,
+ *   camera c skipped for texel i when z <= 0 or det <= 1e-7 (readings M1-M6).
+ * The labels feed render_backward's dynamic_mask (gradient freezing).
+ * masks: device, n_cams*H*W bytes (all cameras share W, H).  labels: device, H_A*W_A bytes,
+ * OVERWRITTEN (1 dynamic / 0 static; unoccupied texels 0).  workspace: device, at least
+ * puv_label_workspace_bytes(W, H) bytes.  r_max >= 0 (SPEC.md:472 default 64). */
+size_t puv_label_workspace_bytes(int32_t width, int32_t height);
+puv_status puv_label_dynamic(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                             int32_t n_cams, const puv_camera* cams, const uint8_t* masks, int32_t r_max,
+                             uint8_t* labels, void* workspace, size_t workspace_bytes, void* stream);
+
 /* The one host synchronisation per step: waits for `stream`, then reports
  * whether any view of the last render overflowed the arena and the arena
  * bytes the call needs.  Host outputs. */
@@ -173,7 +187,7 @@ puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_c
  * device milliseconds, the kernels launched and the number of timed stage
  * instances; kernel_launches counts every kernel the library launched since it
  * was loaded (profiling on or off).  Stages: */
-#define PUV_NUM_STAGES 8
+#define PUV_NUM_STAGES 9
 enum {
   PUV_STAGE_PROJECT = 0,      /* K1 unpack + EWA projection + SH colour + rect (rows a1, a2) */
   PUV_STAGE_DEPTH_SORT = 1,   /* K3 depth radix sort with culling compaction (row a4, low digit) */
@@ -182,7 +196,8 @@ enum {
   PUV_STAGE_LOSS = 4,         /* K10 L2 loss gradient (row a6) */
   PUV_STAGE_RASTER_BWD = 5,   /* K6 composite backward (row a7) */
   PUV_STAGE_PROJECT_BWD = 6,  /* K7 projection + unpack backward, scatter to texels (rows a8, a9) */
-  PUV_STAGE_PACK = 7          /* K9 pack / unpack */
+  PUV_STAGE_PACK = 7,         /* K9 pack / unpack */
+  PUV_STAGE_LABEL = 8         /* K11 flow masking (supp. Alg. 1) */
 };
 typedef struct {
   double ms[PUV_NUM_STAGES];

@@ -474,6 +474,38 @@ puv_status puv_debug_contract(int32_t op, const float* in, float* out, int64_t n
   return cuda_check("puv_debug_contract");
 }
 
+size_t puv_label_workspace_bytes(int32_t width, int32_t height) {
+  if (width < 1 || height < 1) return 0;
+  return (size_t)4 * ((size_t)width + 1) * ((size_t)height + 1);
+}
+
+puv_status puv_label_dynamic(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                             int32_t n_cams, const puv_camera* cams, const uint8_t* masks, int32_t r_max,
+                             uint8_t* labels, void* workspace, size_t workspace_bytes, void* stream) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  if (!atlas_planes || !masks || !labels || !workspace) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
+  for (int d = 0; d < layout->planes; ++d)
+    if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+  if (r_max < 0) return fail(PUV_E_INVALID_ARGUMENT, "r_max %d < 0", r_max);
+  int W, H;
+  st = check_cameras(n_cams, cams, W, H);
+  if (st) return st;
+  if (workspace_bytes < puv_label_workspace_bytes(W, H))
+    return fail(PUV_E_WORKSPACE_TOO_SMALL, "workspace_bytes %zu < %zu", workspace_bytes,
+                puv_label_workspace_bytes(W, H));
+  Plan p{};
+  p.N = layout->atlas_w * layout->atlas_h;
+  PlaneTab P;
+  for (int d = 0; d < layout->planes; ++d) P.p[d] = atlas_planes[d];
+  cudaStream_t s = (cudaStream_t)stream;
+  StageScope sc(PUV_STAGE_LABEL, s);
+  for (int c = 0; c < n_cams; ++c)
+    launch_label(p, P, atlas_occ, cam_dev(cams[c]), masks + (size_t)c * W * H, (uint32_t*)workspace, r_max, c == 0,
+                 labels, s);
+  return cuda_check("puv_label_dynamic");
+}
+
 puv_status puv_profile_enable(int32_t on) {
   g_prof_on = on != 0;
   return PUV_OK;

@@ -110,6 +110,8 @@ void launch_pack(const puv_layout& L, const float* const* level_planes, const ui
                  float* const* atlas_planes, uint8_t* atlas_occ, cudaStream_t s);
 void launch_unpack(const puv_layout& L, const float* const* atlas_planes, float* const* level_planes, cudaStream_t s);
 void launch_contract(int op, const float* in, float* out, int64_t n, cudaStream_t s);
+void launch_label(const Plan& p, const PlaneTab& P, const uint8_t* occ, const CamDev& cam, const uint8_t* mask,
+                  uint32_t* sat, int r_max, int first, uint8_t* labels, cudaStream_t s);
 void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaStream_t s);
 
 }  // namespace puv

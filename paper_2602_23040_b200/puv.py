@@ -59,8 +59,8 @@ class ViewDebug(C.Structure):
                 ("depth_order", C.c_void_p), ("n_examined", C.c_uint64), ("n_composited", C.c_uint64)]
 
 
-NUM_STAGES = 8
-STAGES = ("project", "depth_sort", "bin", "raster_fwd", "loss", "raster_bwd", "project_bwd", "pack")
+NUM_STAGES = 9
+STAGES = ("project", "depth_sort", "bin", "raster_fwd", "loss", "raster_bwd", "project_bwd", "pack", "label")
 
 
 class Profile(C.Structure):
@@ -89,6 +89,10 @@ def lib():
         L.puv_check_overflow.argtypes = [P, S, P, P, P]
         L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
         L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
+        L.puv_label_workspace_bytes.argtypes = [S, S]
+        L.puv_label_workspace_bytes.restype = C.c_size_t
+        L.puv_label_dynamic.argtypes = [P, P, P, S, P, P, S, P, P, C.c_size_t, P]
+        L.puv_label_dynamic.restype = C.c_int32
         L.puv_profile_enable.argtypes = [S]
         L.puv_profile_read.argtypes = [P, S]
         L.puv_profile_enable.restype = C.c_int32
@@ -223,6 +227,24 @@ def render_backward(layout, atlas, occ, cams, opts_, dL, mask, state, arena, gra
     _ok(lib().puv_render_backward(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
                                   C.byref(opts_) if opts_ else None, _ptr(dL), _ptr(mask), _ptr(state),
                                   state.numel(), _ptr(arena), arena.numel(), _planes(grad), _stream(stream)))
+
+
+def label_workspace_bytes(width: int, height: int) -> int:
+    return int(lib().puv_label_workspace_bytes(width, height))
+
+
+def label_dynamic(layout, atlas, occ, cams, masks, r_max=64, labels=None, workspace=None, stream=None):
+    """Supp. Alg. 1 flow masking.  masks: (n_cams, H, W) uint8 CUDA tensor.  Returns labels (H_A, W_A) uint8."""
+    dev = masks.device
+    W, H = cams[0].width, cams[0].height
+    if labels is None:
+        labels = torch.empty((layout.atlas_h, layout.atlas_w), dtype=torch.uint8, device=dev)
+    if workspace is None:
+        workspace = torch.empty(label_workspace_bytes(W, H), dtype=torch.uint8, device=dev)
+    assert masks.dtype == torch.uint8 and masks.is_contiguous() and tuple(masks.shape) == (len(cams), H, W)
+    _ok(lib().puv_label_dynamic(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams, _ptr(masks), int(r_max),
+                                _ptr(labels), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return labels
 
 
 def check_overflow(state, n_views, stream=None):

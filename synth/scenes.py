@@ -273,6 +273,23 @@ def frame_positions(scene: Scene, frame: int) -> np.ndarray:
     return np.ascontiguousarray(mu.T.reshape(3, lv.rows, lv.cols)).astype(np.float32)
 
 
+def motion_masks(scene: Scene, views, n_blobs=6, rmin=0.03, rmax=0.12, tag=2) -> np.ndarray:
+    """Seeded stand-in for thresholded + dilated optical-flow masks (RAFT is out of
+    scope): per view, the union of n_blobs discs with radii U[rmin, rmax] x image height at uniform
+    centres.  Returns (len(views), H, W) uint8 in {0, 1}."""
+    cam0 = scene.cameras[views[0]]
+    H, W = cam0.height, cam0.width
+    out = np.zeros((len(views), H, W), np.uint8)
+    jj, ii = np.mgrid[0:H, 0:W]
+    for k, v in enumerate(views):
+        rng = np.random.default_rng(np.random.SeedSequence([*SEED_ROOT, scene.cfg, tag, v]))
+        for _ in range(n_blobs):
+            cx, cy = rng.uniform(0, W), rng.uniform(0, H)
+            r = rng.uniform(rmin, rmax) * H
+            out[k][(ii - cx) ** 2 + (jj - cy) ** 2 <= r * r] = 1
+    return out
+
+
 # ----------------------------------------------------------------------------
 # tiny hand-built scenes for pins (tests)
 

@@ -48,14 +48,30 @@ __global__ void __launch_bounds__(1024) k_sat_rows(const uint8_t* __restrict__ m
   }
 }
 
-__global__ void k_sat_cols(int W, int H, uint32_t* __restrict__ S) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x > W) return;
-  uint32_t run = 0;
-  for (int y = 1; y <= H; ++y) {
-    uint32_t* p = S + (size_t)y * (W + 1) + x;
-    run += *p;
-    *p = run;
+// Column prefix over rows 1..H: block = 32 columns x 32 warps, warp w owns a chunk of rows.
+__global__ void __launch_bounds__(1024) k_sat_cols(int W, int H, uint32_t* __restrict__ S) {
+  __shared__ uint32_t part[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x = blockIdx.x * 32 + lane;
+  const int per = (H + 31) / 32;
+  const int r0 = 1 + warp * per, r1 = min(H + 1, r0 + per);
+  uint32_t s = 0;
+  if (x <= W)
+    for (int y = r0; y < r1; ++y) s += S[(size_t)y * (W + 1) + x];
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t run = 0;
+    for (int w = 0; w < 32; ++w) { const uint32_t t = part[w][lane]; part[w][lane] = run; run += t; }
+  }
+  __syncthreads();
+  if (x <= W) {
+    uint32_t run = part[warp][lane];
+    for (int y = r0; y < r1; ++y) {
+      uint32_t* p = S + (size_t)y * (W + 1) + x;
+      run += *p;
+      *p = run;
+    }
   }
 }
 
@@ -65,21 +81,60 @@ __device__ __forceinline__ uint32_t sat_count(const uint32_t* S, int W1, int x0,
          S[(size_t)y0 * W1 + x0];
 }
 
+__device__ bool project_window(const PlaneTab& P, int g, const CamDev& cam, int r_max, const uint32_t* S, float& mx,
+                               float& my, float& ha, float& nb, float& hc, int& x0, int& x1, int& y0, int& y1);
+
 __global__ void __launch_bounds__(128) k_label(PlaneTab P, const uint8_t* __restrict__ occ, int N,
                                                const __grid_constant__ CamDev cam, const uint8_t* __restrict__ mask,
                                                const uint32_t* __restrict__ S, int r_max, int first,
                                                uint8_t* __restrict__ labels) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= N) return;
-  if (first) labels[g] = 0;
-  else if (labels[g]) return;                       // OR over cameras: already dynamic
-  if (occ != nullptr && occ[g] == 0) return;
+  const int lane = threadIdx.x & 31;
+  // phase 1 (per lane): projection, validity, window and the O(1) "window holds a mask pixel" test
+  bool cand = false;
+  float mx = 0.f, my = 0.f, ha = 0.f, nb = 0.f, hc = 0.f;
+  int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+  if (g < N) {
+    if (first) labels[g] = 0;
+    cand = (first || !labels[g]) && (occ == nullptr || occ[g] != 0);   // OR over cameras: skip if dynamic
+  }
+  if (cand) cand = project_window(P, g, cam, r_max, S, mx, my, ha, nb, hc, x0, x1, y0, y1);
+  // phase 2 (warp-cooperative): scan the candidate windows one at a time, 32 pixels per step
+  uint32_t todo = __ballot_sync(0xffffffffu, cand);
+  const int W1 = cam.W + 1;
+  while (todo) {
+    const int leader = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const float lmx = __shfl_sync(0xffffffffu, mx, leader), lmy = __shfl_sync(0xffffffffu, my, leader);
+    const float lha = __shfl_sync(0xffffffffu, ha, leader), lnb = __shfl_sync(0xffffffffu, nb, leader);
+    const float lhc = __shfl_sync(0xffffffffu, hc, leader);
+    const int lx0 = __shfl_sync(0xffffffffu, x0, leader), lx1 = __shfl_sync(0xffffffffu, x1, leader);
+    const int ly0 = __shfl_sync(0xffffffffu, y0, leader), ly1 = __shfl_sync(0xffffffffu, y1, leader);
+    bool hit = false;
+    for (int j = ly0; j <= ly1 && !hit; ++j) {
+      if (sat_count(S, W1, lx0, lx1, j, j) == 0) continue;      // no mask pixel in this window row
+      const uint8_t* row = mask + (size_t)j * cam.W;
+      const float fj = (float)j;
+      for (int i0 = lx0; i0 <= lx1 && !hit; i0 += 32) {
+        const int i = i0 + lane;
+        const bool h = i <= lx1 && row[i] && pair_power(lmx, lmy, lha, lnb, lhc, (float)i, fj) >= -4.5f;
+        hit = __any_sync(0xffffffffu, h);
+      }
+    }
+    if (hit && lane == leader) labels[g] = 1;
+  }
+}
+
+// Alg. 1 steps 1-4 for texel g and camera `cam`; returns false when the camera cannot mark the
+// texel (invalid projection, empty window, or no mask pixel inside the window).
+__device__ bool project_window(const PlaneTab& P, int g, const CamDev& cam, int r_max, const uint32_t* S, float& mx,
+                               float& my, float& ha, float& nb, float& hc, int& x0, int& x1, int& y0, int& y1) {
   const Unpacked u = unpack_contract(__ldg(P.p[3] + g), __ldg(P.p[4] + g), __ldg(P.p[5] + g), __ldg(P.p[6] + g),
                                      __ldg(P.p[7] + g), __ldg(P.p[8] + g), __ldg(P.p[9] + g), __ldg(P.p[10] + g));
-  if (!u.ok) return;
+  if (!u.ok) return false;
   const float mux = __ldg(P.p[0] + g), muy = __ldg(P.p[1] + g), muz = __ldg(P.p[2] + g);
   const CamPoint cp = cam_point(cam, mux, muy, muz);
-  if (!(cp.z > 0.0f)) return;                                   // Alg. 1: z <= 0 -> static
+  if (!(cp.z > 0.0f)) return false;                             // Alg. 1: z <= 0 -> static
   // Alg. 1's Jacobian has no clamp: J02 = -fx x / z^2 with the unclamped x/z
   const float J00 = dvd(cam.fx, cp.z), J02 = -dvd(mul(cam.fx, cp.ux), cp.z);
   const float J11 = dvd(cam.fy, cp.z), J12 = -dvd(mul(cam.fy, cp.uy), cp.z);
@@ -98,36 +153,26 @@ __global__ void __launch_bounds__(128) k_label(PlaneTab P, const uint8_t* __rest
   const float b = add(add(mul(T10, W00), mul(T11, W01)), mul(T12, W02));
   const float c = add(add(add(mul(T10, W10), mul(T11, W11)), mul(T12, W12)), 0.3f);
   const float det = sub(mul(a, c), mul(b, b));
-  if (!(det > 1e-7f)) return;
-  const float ha = mul(-0.5f, dvd(c, det)), nb = dvd(b, det), hc = mul(-0.5f, dvd(a, det));
+  if (!(det > 1e-7f)) return false;
+  ha = mul(-0.5f, dvd(c, det));
+  nb = dvd(b, det);
+  hc = mul(-0.5f, dvd(a, det));
   const float tr = add(a, c);
   const float lam = mul(0.5f, add(tr, sqrt_(fmaxf(0.0f, sub(mul(tr, tr), mul(4.0f, det))))));
   const float rf = fminf((float)r_max, ceilf(mul(3.0f, sqrt_(lam))));
-  const float mx = add(mul(cam.fx, cp.ux), cam.cx), my = add(mul(cam.fy, cp.uy), cam.cy);
+  mx = add(mul(cam.fx, cp.ux), cam.cx);
+  my = add(mul(cam.fy, cp.uy), cam.cy);
   const float fx0 = fmaxf(ceilf(sub(mx, rf)), 0.0f), fx1 = fminf(floorf(add(mx, rf)), (float)(cam.W - 1));
   const float fy0 = fmaxf(ceilf(sub(my, rf)), 0.0f), fy1 = fminf(floorf(add(my, rf)), (float)(cam.H - 1));
-  if (fx0 > fx1 || fy0 > fy1) return;
-  const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
-  const int W1 = cam.W + 1;
-  if (sat_count(S, W1, x0, x1, y0, y1) == 0) return;           // no mask pixel in the window
-  for (int j = y0; j <= y1; ++j) {
-    if (sat_count(S, W1, x0, x1, j, j) == 0) continue;         // no mask pixel in this row of the window
-    const uint8_t* row = mask + (size_t)j * cam.W;
-    const float fj = (float)j;
-    for (int i = x0; i <= x1; ++i) {
-      if (!row[i]) continue;
-      if (pair_power(mx, my, ha, nb, hc, (float)i, fj) >= -4.5f) {
-        labels[g] = 1;
-        return;
-      }
-    }
-  }
+  if (fx0 > fx1 || fy0 > fy1) return false;
+  x0 = (int)fx0; x1 = (int)fx1; y0 = (int)fy0; y1 = (int)fy1;
+  return sat_count(S, cam.W + 1, x0, x1, y0, y1) != 0;          // any mask pixel in the window?
 }
 
 void launch_label(const Plan& p, const PlaneTab& P, const uint8_t* occ, const CamDev& cam, const uint8_t* mask,
                   uint32_t* sat, int r_max, int first, uint8_t* labels, cudaStream_t s) {
   k_sat_rows<<<cam.H + 1, 1024, 0, s>>>(mask, cam.W, cam.H, sat);
-  k_sat_cols<<<(cam.W + 1 + 255) / 256, 256, 0, s>>>(cam.W, cam.H, sat);
+  k_sat_cols<<<(cam.W + 1 + 31) / 32, 1024, 0, s>>>(cam.W, cam.H, sat);
   k_label<<<(p.N + 127) / 128, 128, 0, s>>>(P, occ, p.N, cam, mask, sat, r_max, first, labels);
   count_launches(3);
 }

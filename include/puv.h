@@ -69,7 +69,18 @@ typedef struct {
   int32_t planes;       /* D = 11 + 3*(sh_degree+1)^2 */
   int32_t atlas_w, atlas_h;
   puv_placement level[PUV_MAX_LEVELS];
+  /* Position storage:
+   *  PUV_POS_XYZ: planes 0..2 hold the world position (default).
+   *  PUV_POS_RHO: plane 0 holds rho, the distance from `center` along the texel's UV ray; planes 1..2
+   *    are unused (their table entries may be NULL and their gradients are left untouched) and the
+   *    plane table passed to render/backward has D + 3 entries: [D..D+2] = the ray-direction planes
+   *    written by puv_ray_planes.  The texel position is mu = center (+) rho (x) ray in the fp32
+   *    contract; d rho = ray . d mu. */
+  int32_t position_mode;
+  float center[3];
 } puv_layout;
+
+enum { PUV_POS_XYZ = 0, PUV_POS_RHO = 1 };
 
 /* Pinhole camera, OpenCV axes (x right, y down, z forward) (R4).  Pixel (i, j)
  * is sampled at integer coordinates. */
@@ -91,6 +102,22 @@ typedef struct {
  * rows/cols: host arrays of K.  out: host. */
 puv_status puv_layout_for_levels(int32_t K, const int32_t* rows, const int32_t* cols, int32_t sh_degree,
                                  puv_layout* out);
+
+/* The paper's pyramid schedule and recursive atlas layout: level 0
+ * is M0 x N0 and levels alternate halving N and M (odd k: N/2, even k: M/2).  A level is an image of
+ * M_k columns (u, azimuth) by N_k rows (v, polar).  Placement (x, y of the top-left corner): L0 at
+ * (S/2, 0); L1 rotated 90 deg CCW at (0, 0); L2 at (0, S); L3 (rotated) right of L2, L4 right of L3,
+ * L5 (rotated) below L4, L6 right of L5, L7 (rotated) below L6 — odd levels rotated, even levels not.
+ * M0 = N0 = S (a power of two >= 16), 1 <= K <= 8.  For S = 1024, K = 8: atlas 1536 x 1536 with
+ * 2,088,960 used texels (0.8854, "88.5% efficiency").  position_mode = PUV_POS_XYZ. */
+puv_status puv_layout_paper(int32_t S, int32_t K, int32_t sh_degree, puv_layout* out);
+
+/* Ray-direction planes of an atlas (for PUV_POS_RHO): for level k cell (v = row, u = column),
+ * theta = (u + 0.5)/M_k 2 pi - pi, phi = (v + 0.5)/N_k pi, ray = (sin phi cos theta, sin phi sin theta,
+ * cos phi) (the inverse of PAPER.md eq. uvgs2 at pixel centres), evaluated in fp64 on
+ * the host and rounded to fp32, written at the texel's atlas position; unplaced texels get 0.
+ * ray_planes: host array of 3 device pointers (H_A*W_A floats each).  Synchronous. */
+puv_status puv_ray_planes(const puv_layout* layout, float* const* ray_planes, void* stream);
 
 /* Pack K levels into the atlas.  level_planes: host array of
  * K*D device pointers, k-major (level k plane d at [k*D + d]), each rows_k*cols_k

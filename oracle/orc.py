@@ -69,6 +69,10 @@ def lib():
         L.orc_backward.argtypes = [P, P, C.c_int, C.c_int64, P, P, P, P, P, P]
         L.orc_layout_column.argtypes = [C.c_int, P, P, P, P, P]
         L.orc_label_dynamic.argtypes = [P, C.c_int64, P, C.c_int, P, P, C.c_int, P, C.c_int64, P]
+        L.orc_layout_paper.argtypes = [C.c_int, C.c_int, P, P, P, P, P]
+        L.orc_ray_dirs.argtypes = [C.c_int, P, P, P, C.c_int32, C.c_int32, P, P, P]
+        L.orc_positions_from_rho.argtypes = [P, P, P, P, P, C.c_int64, P, P, P]
+        L.orc_rho_grad.argtypes = [P, P, P, P, P, P, C.c_int64, P]
         L.orc_pack.argtypes = [C.c_int, P, P, P, C.c_int, P, P, C.c_int32, C.c_int32, P, P]
         _LIB = L
     return _LIB
@@ -131,6 +135,49 @@ def layout_column(shapes):
     rc = lib().orc_layout_column(K, _ptr(rows), _ptr(cols), _ptr(place), C.byref(W), C.byref(H))
     assert rc == 0
     return place, W.value, H.value
+
+
+def layout_paper(S, K):
+    """(rows, cols, place (K,3), W, H) of the paper's K-level pyramid atlas."""
+    rows = np.zeros(K, np.int32)
+    cols = np.zeros(K, np.int32)
+    place = np.zeros((K, 3), np.int32)
+    W = C.c_int32()
+    H = C.c_int32()
+    rc = lib().orc_layout_paper(S, K, _ptr(rows), _ptr(cols), _ptr(place), C.byref(W), C.byref(H))
+    assert rc == 0
+    return rows, cols, place, W.value, H.value
+
+
+def ray_dirs(rows, cols, place, W, H):
+    """(3, H, W) fp32 ray direction of every atlas texel (0 where unplaced)."""
+    out = np.zeros((3, H, W), np.float32)
+    r = np.ascontiguousarray(rows, np.int32)
+    c = np.ascontiguousarray(cols, np.int32)
+    p = np.ascontiguousarray(place, np.int32)
+    lib().orc_ray_dirs(len(r), _ptr(r), _ptr(c), _ptr(p), W, H, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]))
+    return out
+
+
+def positions_from_rho(rho, rays, center):
+    """mu = c (+) rho (x) ray in fp32.  rho (H, W); rays (3, H, W) -> (3, H, W)."""
+    rho = np.ascontiguousarray(rho, np.float32)
+    rays = np.ascontiguousarray(rays, np.float32)
+    c = np.asarray(center, np.float32)
+    out = np.empty((3,) + rho.shape, np.float32)
+    lib().orc_positions_from_rho(_ptr(rho), _ptr(rays[0]), _ptr(rays[1]), _ptr(rays[2]), _ptr(c), rho.size,
+                                 _ptr(out[0]), _ptr(out[1]), _ptr(out[2]))
+    return out
+
+
+def rho_grad(rays, gxyz):
+    """d rho = ray . d mu (fp64)."""
+    rays = np.ascontiguousarray(rays, np.float32)
+    g = np.ascontiguousarray(gxyz, np.float64)
+    out = np.empty(rays.shape[1:], np.float64)
+    lib().orc_rho_grad(_ptr(rays[0]), _ptr(rays[1]), _ptr(rays[2]), _ptr(g[0]), _ptr(g[1]), _ptr(g[2]),
+                       out.size, _ptr(out))
+    return out
 
 
 def pack(levels, place=None, W=None, H=None):

@@ -835,6 +835,79 @@ int orc_layout_column(int K, const int32_t* rows, const int32_t* cols, int32_t* 
     return 0;
 }
 
+/* The paper's K <= 8 pyramid atlas as the placement table of
+ * scaled by S/1024 (levels: image of M_k = cols columns, N_k = rows rows; odd levels rotated):
+ *   k  (M_k, N_k)        x, y (top-left)     rotated
+ *   0  (S, S)            (S/2, 0)            no
+ *   1  (S, S/2)          (0, 0)              yes
+ *   2  (S/2, S/2)        (0, S)              no
+ *   3  (S/2, S/4)        (S/2, S)            yes
+ *   4  (S/4, S/4)        (3S/4, S)           no
+ *   5  (S/4, S/8)        (3S/4, 5S/4)        yes
+ *   6  (S/8, S/8)        (7S/8, 5S/4)        no
+ *   7  (S/8, S/16)       (7S/8, 11S/8)       yes
+ * atlas (3S/2)^2 for K >= 3, 3S/2 x S for K = 2, S x S for K = 1 (L0 then at (0,0)).
+ * out: K x {x, y, rot}; rows/cols: K each. */
+int orc_layout_paper(int S, int K, int32_t* rows, int32_t* cols, int32_t* out, int32_t* W, int32_t* H)
+{
+    static const int M8[8] = {8, 8, 4, 4, 2, 2, 1, 1};      /* in units of S/8 */
+    static const int N16[8] = {16, 8, 8, 4, 4, 2, 2, 1};    /* in units of S/16 */
+    static const int X8[8] = {4, 0, 0, 4, 6, 6, 7, 7};      /* x in units of S/8 */
+    static const int Y8[8] = {0, 0, 8, 8, 8, 10, 10, 11};   /* y in units of S/8 */
+    if (K < 1 || K > 8 || S < 16 || (S & (S - 1))) return -2;
+    for (int k = 0; k < K; ++k) {
+        cols[k] = M8[k] * (S / 8);
+        rows[k] = N16[k] * (S / 16);
+        out[3 * k] = (K == 1) ? 0 : X8[k] * (S / 8);
+        out[3 * k + 1] = Y8[k] * (S / 8);
+        out[3 * k + 2] = k & 1;
+    }
+    *W = K > 1 ? S + S / 2 : S;
+    *H = K > 2 ? S + S / 2 : S;
+    return 0;
+}
+
+/* Ray direction of every atlas texel (zero where unplaced): level cell (v = row, u = column),
+ * theta = (u + 0.5)/M 2pi - pi, phi = (v + 0.5)/N pi (inverse of PAPER.md eq. uvgs2 at pixel
+ * centres), dir = (sin phi cos theta, sin phi sin theta, cos phi) in fp64, rounded. */
+int orc_ray_dirs(int K, const int32_t* rows, const int32_t* cols, const int32_t* place, int32_t W_A, int32_t H_A,
+                 float* rx, float* ry, float* rz)
+{
+    const double pi = 3.14159265358979323846;
+    int64_t NA = (int64_t)W_A * H_A;
+    memset(rx, 0, (size_t)NA * 4); memset(ry, 0, (size_t)NA * 4); memset(rz, 0, (size_t)NA * 4);
+    for (int k = 0; k < K; ++k)
+        for (int r = 0; r < rows[k]; ++r)
+            for (int c = 0; c < cols[k]; ++c) {
+                double th = (c + 0.5) / cols[k] * 2.0 * pi - pi, ph = (r + 0.5) / rows[k] * pi;
+                int64_t ay = place[3 * k + 2] ? place[3 * k + 1] + cols[k] - 1 - c : place[3 * k + 1] + r;
+                int64_t ax = place[3 * k + 2] ? place[3 * k] + r : place[3 * k] + c;
+                int64_t o = ay * W_A + ax;
+                rx[o] = (float)(sin(ph) * cos(th));
+                ry[o] = (float)(sin(ph) * sin(th));
+                rz[o] = (float)cos(ph);
+            }
+    return 0;
+}
+
+/* PUV_POS_RHO positions: mu_k = c_k (+) rho (x) ray_k in fp32 (two IEEE ops). */
+void orc_positions_from_rho(const float* rho, const float* rx, const float* ry, const float* rz, const float* c,
+                            int64_t n, float* x, float* y, float* z)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = c[0] + rho[i] * rx[i];
+        y[i] = c[1] + rho[i] * ry[i];
+        z[i] = c[2] + rho[i] * rz[i];
+    }
+}
+
+/* d rho = ray . d mu (fp64) */
+void orc_rho_grad(const float* rx, const float* ry, const float* rz, const double* gx, const double* gy,
+                  const double* gz, int64_t n, double* grho)
+{
+    for (int64_t i = 0; i < n; ++i) grho[i] = (double)rx[i] * gx[i] + (double)ry[i] * gy[i] + (double)rz[i] * gz[i];
+}
+
 /* Level k (rows_k x cols_k, D planes) -> atlas (H_A x W_A).  Unrotated: cell
  * (r, c) -> (y + r, x + c).  rot90ccw: placement is cols_k tall, rows_k wide
  * and cell (r, c) -> (y + cols_k - 1 - c, x + r).  Unplaced pixels: zero and

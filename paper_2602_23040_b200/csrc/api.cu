@@ -117,6 +117,8 @@ static puv_status check_layout(const puv_layout* L) {
   if (L->planes != D) return fail(PUV_E_DIMENSION_MISMATCH, "planes %d != 11 + 3 (deg+1)^2 = %d", L->planes, D);
   if (L->atlas_w < 1 || L->atlas_h < 1 || (int64_t)L->atlas_w * L->atlas_h >= (int64_t)1 << 31)
     return fail(PUV_E_INVALID_CONFIG, "atlas %d x %d", L->atlas_w, L->atlas_h);
+  if (L->position_mode != PUV_POS_XYZ && L->position_mode != PUV_POS_RHO)
+    return fail(PUV_E_INVALID_CONFIG, "position_mode %d", L->position_mode);
   for (int k = 0; k < L->num_levels; ++k) {
     const puv_placement& a = L->level[k];
     if (a.rows < 1 || a.cols < 1) return fail(PUV_E_INVALID_CONFIG, "level %d is empty", k);
@@ -183,6 +185,9 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.ntiles = p.gx * p.gy;
   p.D = L.planes;
   p.deg = L.sh_degree;
+  p.pm.rho = L.position_mode == PUV_POS_RHO;
+  p.pm.D = L.planes;
+  for (int k = 0; k < 3; ++k) p.pm.c[k] = L.center[k];
   const size_t V = n_views, N = p.N;
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off += align_up(bytes); return o; };
@@ -245,14 +250,27 @@ struct Common {
   int W, H;
 };
 
+// Plane table of a render/backward/label call: D entries, + the 3 ray planes in PUV_POS_RHO mode
+// (where entries 1 and 2 are unused and may be NULL).
+static puv_status fill_planes(const puv_layout* L, const float* const* tab, PlaneTab& P) {
+  if (!tab) return fail(PUV_E_INVALID_ARGUMENT, "atlas_planes is NULL");
+  const bool rho = L->position_mode == PUV_POS_RHO;
+  const int n = L->planes + (rho ? 3 : 0);
+  for (int d = 0; d < n; ++d) {
+    if (rho && (d == 1 || d == 2)) { P.p[d] = nullptr; continue; }
+    if (!tab[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+    P.p[d] = tab[d];
+  }
+  return PUV_OK;
+}
+
 static puv_status prepare(const puv_layout* L, const float* const* atlas_planes, int32_t n_views,
                           const puv_camera* cams, const puv_render_opts* opts, void* state, size_t state_bytes,
                           Common& c) {
   puv_status st = check_layout(L);
   if (st) return st;
-  if (!atlas_planes) return fail(PUV_E_INVALID_ARGUMENT, "atlas_planes is NULL");
-  for (int d = 0; d < L->planes; ++d)
-    if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+  st = fill_planes(L, atlas_planes, c.P);
+  if (st) return st;
   if (opts && opts->flags != 0) return fail(PUV_E_UNSUPPORTED, "opts.flags must be 0");
   st = check_cameras(n_views, cams, c.W, c.H);
   if (st) return st;
@@ -261,7 +279,6 @@ static puv_status prepare(const puv_layout* L, const float* const* atlas_planes,
   if (state_bytes < c.plan.total)
     return fail(PUV_E_WORKSPACE_TOO_SMALL, "state_bytes %zu < %zu", state_bytes, c.plan.total);
   c.views = views_of(c.plan, state);
-  for (int d = 0; d < L->planes; ++d) c.P.p[d] = atlas_planes[d];
   return PUV_OK;
 }
 
@@ -299,6 +316,70 @@ puv_status puv_layout_for_levels(int32_t K, const int32_t* rows, const int32_t* 
   L.atlas_w = (int32_t)W;
   L.atlas_h = (int32_t)H;
   *out = L;
+  return PUV_OK;
+}
+
+puv_status puv_layout_paper(int32_t S, int32_t K, int32_t sh_degree, puv_layout* out) {
+  if (!out) return fail(PUV_E_INVALID_ARGUMENT, "NULL output");
+  if (K < 1 || K > 8) return fail(PUV_E_INVALID_CONFIG, "K %d outside 1..8", K);
+  if (S < 16 || (S & (S - 1))) return fail(PUV_E_INVALID_CONFIG, "S %d must be a power of two >= 16", S);
+  if (sh_degree < 0 || sh_degree > PUV_MAX_SH_DEGREE) return fail(PUV_E_INVALID_CONFIG, "sh_degree %d", sh_degree);
+  puv_layout L;
+  std::memset(&L, 0, sizeof L);
+  L.num_levels = K;
+  L.sh_degree = sh_degree;
+  L.planes = 11 + 3 * (sh_degree + 1) * (sh_degree + 1);
+  // schedule: (M_k, N_k) = (M, N/2) for odd k, (M/2, N) for even k; level = N rows x M cols
+  int M = S, Nn = S;
+  int px = 0, py = 0, pw = 0, ph = 0;   // previous placement (x, y, width, height)
+  for (int k = 0; k < K; ++k) {
+    if (k > 0) { if (k & 1) Nn /= 2; else M /= 2; }
+    puv_placement& a = L.level[k];
+    a.rows = Nn;
+    a.cols = M;
+    a.rot90ccw = k & 1;
+    const int w = a.rot90ccw ? a.rows : a.cols, h = a.rot90ccw ? a.cols : a.rows;
+    if (k == 0) { a.x = K > 1 ? S / 2 : 0; a.y = 0; }
+    else if (k == 1) { a.x = 0; a.y = 0; }
+    else if (k == 2) { a.x = 0; a.y = S; }
+    else if (k == 3 || k == 4 || k == 6) { a.x = px + pw; a.y = py; }      // right of the previous level
+    else { a.x = px; a.y = py + ph; }                                      // k = 5, 7: below the previous
+    px = a.x; py = a.y; pw = w; ph = h;
+  }
+  L.atlas_w = K > 1 ? S + S / 2 : S;
+  L.atlas_h = K > 2 ? S + S / 2 : S;
+  const puv_status st = check_layout(&L);
+  if (st) return st;
+  *out = L;
+  return PUV_OK;
+}
+
+puv_status puv_ray_planes(const puv_layout* layout, float* const* ray_planes, void* stream) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  if (!ray_planes || !ray_planes[0] || !ray_planes[1] || !ray_planes[2])
+    return fail(PUV_E_INVALID_ARGUMENT, "NULL ray plane");
+  const size_t NA = (size_t)layout->atlas_w * layout->atlas_h;
+  std::vector<float> host(3 * NA, 0.0f);
+  const double kPi = 3.14159265358979323846;
+  for (int k = 0; k < layout->num_levels; ++k) {
+    const puv_placement& a = layout->level[k];
+    for (int r = 0; r < a.rows; ++r)
+      for (int c = 0; c < a.cols; ++c) {
+        // level image: u = column (azimuth, M_k = cols), v = row (polar, N_k = rows); pixel centres
+        const double theta = (c + 0.5) / a.cols * 2.0 * kPi - kPi, phi = (r + 0.5) / a.rows * kPi;
+        const size_t ay = a.rot90ccw ? (size_t)(a.y + a.cols - 1 - c) : (size_t)(a.y + r);
+        const size_t ax = a.rot90ccw ? (size_t)(a.x + r) : (size_t)(a.x + c);
+        const size_t o = ay * layout->atlas_w + ax;
+        host[o] = (float)(std::sin(phi) * std::cos(theta));
+        host[NA + o] = (float)(std::sin(phi) * std::sin(theta));
+        host[2 * NA + o] = (float)std::cos(phi);
+      }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int d = 0; d < 3; ++d) cudaMemcpyAsync(ray_planes[d], host.data() + d * NA, NA * 4, cudaMemcpyHostToDevice, s);
+  const cudaError_t e = cudaStreamSynchronize(s);   // host staging buffer must outlive the copies
+  if (e != cudaSuccess) return fail(PUV_E_CUDA, "puv_ray_planes: %s", cudaGetErrorString(e));
   return PUV_OK;
 }
 
@@ -401,6 +482,7 @@ puv_status puv_render_backward(const puv_layout* layout, const float* const* atl
   if (!dL_dimages || !atlas_grad) return fail(PUV_E_INVALID_ARGUMENT, "NULL dL_dimages / atlas_grad");
   GradTab G;
   for (int d = 0; d < layout->planes; ++d) {
+    if (layout->position_mode == PUV_POS_RHO && (d == 1 || d == 2)) { G.p[d] = nullptr; continue; }
     if (!atlas_grad[d]) return fail(PUV_E_INVALID_ARGUMENT, "grad plane %d is NULL", d);
     G.p[d] = atlas_grad[d];
   }
@@ -484,9 +566,10 @@ puv_status puv_label_dynamic(const puv_layout* layout, const float* const* atlas
                              uint8_t* labels, void* workspace, size_t workspace_bytes, void* stream) {
   puv_status st = check_layout(layout);
   if (st) return st;
-  if (!atlas_planes || !masks || !labels || !workspace) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
-  for (int d = 0; d < layout->planes; ++d)
-    if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+  if (!masks || !labels || !workspace) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
+  PlaneTab P;
+  st = fill_planes(layout, atlas_planes, P);
+  if (st) return st;
   if (r_max < 0) return fail(PUV_E_INVALID_ARGUMENT, "r_max %d < 0", r_max);
   int W, H;
   st = check_cameras(n_cams, cams, W, H);
@@ -496,8 +579,9 @@ puv_status puv_label_dynamic(const puv_layout* layout, const float* const* atlas
                 puv_label_workspace_bytes(W, H));
   Plan p{};
   p.N = layout->atlas_w * layout->atlas_h;
-  PlaneTab P;
-  for (int d = 0; d < layout->planes; ++d) P.p[d] = atlas_planes[d];
+  p.pm.rho = layout->position_mode == PUV_POS_RHO;
+  p.pm.D = layout->planes;
+  for (int k = 0; k < 3; ++k) p.pm.c[k] = layout->center[k];
   cudaStream_t s = (cudaStream_t)stream;
   StageScope sc(PUV_STAGE_LABEL, s);
   for (int c = 0; c < n_cams; ++c)

@@ -8,7 +8,7 @@
 
 namespace puv {
 
-constexpr int kMaxPlanes = 11 + 3 * 16;   // SH degree 3
+constexpr int kMaxPlanes = 11 + 3 * 16 + 3;   // SH degree 3 + the 3 ray planes of PUV_POS_RHO
 constexpr int kCamBatch = 64;             // views per K1/K7 launch (cameras passed by value, 6 KB of params)
 constexpr int kTile = PUV_TILE;
 constexpr int kNbMax = 1024;              // max key blocks of the stable tile pass per view
@@ -28,6 +28,10 @@ struct CamDev {
   float limx, limy;
 };
 struct CamBatch { CamDev c[kCamBatch]; int n; int v0; };
+
+// Position storage (puv_layout.position_mode): rho mode reads mu = c (+) rho (x) ray with the ray in
+// planes [D, D+3) of the plane table.
+struct PosMode { int rho; int D; float c[3]; };
 
 // Device header of one view (written by kernels; read by later kernels and by the host once per step).
 struct ViewHdr {
@@ -54,6 +58,7 @@ struct CallHdr {
 // Offsets (bytes) of every array inside the caller's state buffer.
 struct Plan {
   int n_views, N, W, H, HW, gx, gy, ntiles, D, deg;
+  PosMode pm;
   size_t call_hdr, view_hdr;
   // per view arrays, each [n_views][...]
   size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull;

@@ -81,10 +81,10 @@ __device__ __forceinline__ uint32_t sat_count(const uint32_t* S, int W1, int x0,
          S[(size_t)y0 * W1 + x0];
 }
 
-__device__ bool project_window(const PlaneTab& P, int g, const CamDev& cam, int r_max, const uint32_t* S, float& mx,
+__device__ bool project_window(const PlaneTab& P, const PosMode& pm, int g, const CamDev& cam, int r_max, const uint32_t* S, float& mx,
                                float& my, float& ha, float& nb, float& hc, int& x0, int& x1, int& y0, int& y1);
 
-__global__ void __launch_bounds__(128) k_label(PlaneTab P, const uint8_t* __restrict__ occ, int N,
+__global__ void __launch_bounds__(128) k_label(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ, int N,
                                                const __grid_constant__ CamDev cam, const uint8_t* __restrict__ mask,
                                                const uint32_t* __restrict__ S, int r_max, int first,
                                                uint8_t* __restrict__ labels) {
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(128) k_label(PlaneTab P, const uint8_t* __rest
     if (first) labels[g] = 0;
     cand = (first || !labels[g]) && (occ == nullptr || occ[g] != 0);   // OR over cameras: skip if dynamic
   }
-  if (cand) cand = project_window(P, g, cam, r_max, S, mx, my, ha, nb, hc, x0, x1, y0, y1);
+  if (cand) cand = project_window(P, pm, g, cam, r_max, S, mx, my, ha, nb, hc, x0, x1, y0, y1);
   // phase 2 (warp-cooperative): scan the candidate windows one at a time, 32 pixels per step
   uint32_t todo = __ballot_sync(0xffffffffu, cand);
   const int W1 = cam.W + 1;
@@ -127,12 +127,13 @@ __global__ void __launch_bounds__(128) k_label(PlaneTab P, const uint8_t* __rest
 
 // Alg. 1 steps 1-4 for texel g and camera `cam`; returns false when the camera cannot mark the
 // texel (invalid projection, empty window, or no mask pixel inside the window).
-__device__ bool project_window(const PlaneTab& P, int g, const CamDev& cam, int r_max, const uint32_t* S, float& mx,
+__device__ bool project_window(const PlaneTab& P, const PosMode& pm, int g, const CamDev& cam, int r_max, const uint32_t* S, float& mx,
                                float& my, float& ha, float& nb, float& hc, int& x0, int& x1, int& y0, int& y1) {
   const Unpacked u = unpack_contract(__ldg(P.p[3] + g), __ldg(P.p[4] + g), __ldg(P.p[5] + g), __ldg(P.p[6] + g),
                                      __ldg(P.p[7] + g), __ldg(P.p[8] + g), __ldg(P.p[9] + g), __ldg(P.p[10] + g));
   if (!u.ok) return false;
-  const float mux = __ldg(P.p[0] + g), muy = __ldg(P.p[1] + g), muz = __ldg(P.p[2] + g);
+  float mux, muy, muz;
+  texel_mu(P, pm, g, mux, muy, muz);
   const CamPoint cp = cam_point(cam, mux, muy, muz);
   if (!(cp.z > 0.0f)) return false;                             // Alg. 1: z <= 0 -> static
   // Alg. 1's Jacobian has no clamp: J02 = -fx x / z^2 with the unclamped x/z
@@ -173,7 +174,7 @@ void launch_label(const Plan& p, const PlaneTab& P, const uint8_t* occ, const Ca
                   uint32_t* sat, int r_max, int first, uint8_t* labels, cudaStream_t s) {
   k_sat_rows<<<cam.H + 1, 1024, 0, s>>>(mask, cam.W, cam.H, sat);
   k_sat_cols<<<(cam.W + 1 + 31) / 32, 1024, 0, s>>>(cam.W, cam.H, sat);
-  k_label<<<(p.N + 127) / 128, 128, 0, s>>>(P, occ, p.N, cam, mask, sat, r_max, first, labels);
+  k_label<<<(p.N + 127) / 128, 128, 0, s>>>(P, p.pm, occ, p.N, cam, mask, sat, r_max, first, labels);
   count_launches(3);
 }
 

@@ -12,13 +12,14 @@
 namespace puv {
 
 template <int DEG>
-__global__ void __launch_bounds__(128) k_project(PlaneTab P, const uint8_t* __restrict__ occ, int N,
+__global__ void __launch_bounds__(128) k_project(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ, int N,
                                                  const __grid_constant__ CamBatch cb, Views v, int gx, int gy) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= N) return;
   constexpr int NK = (DEG + 1) * (DEG + 1);
   const bool occupied = occ == nullptr || occ[g] != 0;
-  const float mux = __ldg(P.p[0] + g), muy = __ldg(P.p[1] + g), muz = __ldg(P.p[2] + g);
+  float mux = 0.f, muy = 0.f, muz = 0.f;
+  if (occupied) texel_mu(P, pm, g, mux, muy, muz);
   const float ls0 = __ldg(P.p[3] + g), ls1 = __ldg(P.p[4] + g), ls2 = __ldg(P.p[5] + g);
   const float qw = __ldg(P.p[6] + g), qx = __ldg(P.p[7] + g), qy = __ldg(P.p[8] + g), qz = __ldg(P.p[9] + g);
   const float logit = __ldg(P.p[10] + g);
@@ -89,10 +90,10 @@ void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint
   const int threads = 128;
   const int blocks = (p.N + threads - 1) / threads;
   switch (p.deg) {
-    case 0: k_project<0><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
-    case 1: k_project<1><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
-    case 2: k_project<2><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
-    default: k_project<3><<<blocks, threads, 0, s>>>(P, occ, p.N, cb, v, p.gx, p.gy); break;
+    case 0: k_project<0><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
+    case 1: k_project<1><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
+    case 2: k_project<2><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
+    default: k_project<3><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
   }
   count_launches(1);
 }

@@ -16,7 +16,7 @@
 namespace puv {
 
 template <int DEG>
-__global__ void __launch_bounds__(128) k_project_bwd(PlaneTab P, const uint8_t* __restrict__ occ,
+__global__ void __launch_bounds__(128) k_project_bwd(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ,
                                                     const uint8_t* __restrict__ mask, int N,
                                                     const __grid_constant__ CamBatch cb, Views v, GradTab Gt) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(128) k_project_bwd(PlaneTab P, const uint8_t* 
   for (int i = 0; i < cb.n; ++i) any |= v.depth[(size_t)(cb.v0 + i) * N + g] != kInvisible;
   if (!any) return;
 
-  const float fmx = __ldg(P.p[0] + g), fmy = __ldg(P.p[1] + g), fmz = __ldg(P.p[2] + g);
+  float fmx, fmy, fmz;
+  texel_mu(P, pm, g, fmx, fmy, fmz);   // the fp32 position the render saw (xyz or c (+) rho (x) ray)
   const double mux = fmx, muy = fmy, muz = fmz;
   const float ls0 = __ldg(P.p[3] + g), ls1 = __ldg(P.p[4] + g), ls2 = __ldg(P.p[5] + g);
   const float qw = __ldg(P.p[6] + g), qx = __ldg(P.p[7] + g), qy = __ldg(P.p[8] + g), qz = __ldg(P.p[9] + g);
@@ -152,9 +153,14 @@ __global__ void __launch_bounds__(128) k_project_bwd(PlaneTab P, const uint8_t* 
   const double dqz = 2 * (-2 * z * dR00 - w * dR01 + x * dR02 + w * dR10 - 2 * z * dR11 + y * dR12 + x * dR20 + y * dR21);
   const double qd = w * dqw + x * dqx + y * dqy + z * dqz;
   if (mask != nullptr && mask[g] == 0) return;   // gradient freezing: D_i = 0
-  Gt.p[0][g] += (float)dmu0;
-  Gt.p[1][g] += (float)dmu1;
-  Gt.p[2][g] += (float)dmu2;
+  if (pm.rho) {   // d rho = ray . d mu, in fp64 before the one rounding (planes 1, 2 untouched)
+    Gt.p[0][g] += (float)((double)__ldg(P.p[pm.D] + g) * dmu0 + (double)__ldg(P.p[pm.D + 1] + g) * dmu1 +
+                          (double)__ldg(P.p[pm.D + 2] + g) * dmu2);
+  } else {
+    Gt.p[0][g] += (float)dmu0;
+    Gt.p[1][g] += (float)dmu1;
+    Gt.p[2][g] += (float)dmu2;
+  }
   Gt.p[3][g] += (float)(2 * t0 * dt0);
   Gt.p[4][g] += (float)(2 * t1 * dt1);
   Gt.p[5][g] += (float)(2 * t2 * dt2);
@@ -172,10 +178,10 @@ void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const 
   const int threads = 128;
   const int blocks = (p.N + threads - 1) / threads;
   switch (p.deg) {
-    case 0: k_project_bwd<0><<<blocks, threads, 0, s>>>(P, occ, mask, p.N, cb, v, G); break;
-    case 1: k_project_bwd<1><<<blocks, threads, 0, s>>>(P, occ, mask, p.N, cb, v, G); break;
-    case 2: k_project_bwd<2><<<blocks, threads, 0, s>>>(P, occ, mask, p.N, cb, v, G); break;
-    default: k_project_bwd<3><<<blocks, threads, 0, s>>>(P, occ, mask, p.N, cb, v, G); break;
+    case 0: k_project_bwd<0><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
+    case 1: k_project_bwd<1><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
+    case 2: k_project_bwd<2><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
+    default: k_project_bwd<3><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
   }
   count_launches(1);
 }

@@ -11,6 +11,20 @@
 
 namespace puv {
 
+// Texel position (a1): explicit xyz planes, or mu = c (+) rho (x) ray in the fp32 contract (PUV_POS_RHO).
+PUV_DEV void texel_mu(const PlaneTab& P, const PosMode& pm, int g, float& x, float& y, float& z) {
+  if (pm.rho) {
+    const float r = __ldg(P.p[0] + g);
+    x = add(pm.c[0], mul(r, __ldg(P.p[pm.D] + g)));
+    y = add(pm.c[1], mul(r, __ldg(P.p[pm.D + 1] + g)));
+    z = add(pm.c[2], mul(r, __ldg(P.p[pm.D + 2] + g)));
+  } else {
+    x = __ldg(P.p[0] + g);
+    y = __ldg(P.p[1] + g);
+    z = __ldg(P.p[2] + g);
+  }
+}
+
 struct Unpacked {
   float S00, S01, S02, S11, S12, S22;  // world covariance (U4)
   float o, t_g;                        // opacity (U5) and log-threshold

@@ -38,7 +38,11 @@ class Placement(C.Structure):
 
 class Layout(C.Structure):
     _fields_ = [("num_levels", C.c_int32), ("sh_degree", C.c_int32), ("planes", C.c_int32),
-                ("atlas_w", C.c_int32), ("atlas_h", C.c_int32), ("level", Placement * MAX_LEVELS)]
+                ("atlas_w", C.c_int32), ("atlas_h", C.c_int32), ("level", Placement * MAX_LEVELS),
+                ("position_mode", C.c_int32), ("center", C.c_float * 3)]
+
+
+POS_XYZ, POS_RHO = 0, 1
 
 
 class Camera(C.Structure):
@@ -89,6 +93,10 @@ def lib():
         L.puv_check_overflow.argtypes = [P, S, P, P, P]
         L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
         L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
+        L.puv_layout_paper.argtypes = [S, S, S, P]
+        L.puv_layout_paper.restype = C.c_int32
+        L.puv_ray_planes.argtypes = [P, P, P]
+        L.puv_ray_planes.restype = C.c_int32
         L.puv_label_workspace_bytes.argtypes = [S, S]
         L.puv_label_workspace_bytes.restype = C.c_size_t
         L.puv_label_dynamic.argtypes = [P, P, P, S, P, P, S, P, P, C.c_size_t, P]
@@ -182,6 +190,33 @@ def layout_for_levels(shapes, sh_degree: int) -> Layout:
     out = Layout()
     _ok(lib().puv_layout_for_levels(K, rows, cols, sh_degree, C.byref(out)))
     return out
+
+
+def layout_paper(S: int, K: int, sh_degree: int) -> Layout:
+    """The paper's pyramid schedule + recursive atlas layout."""
+    out = Layout()
+    _ok(lib().puv_layout_paper(S, K, sh_degree, C.byref(out)))
+    return out
+
+
+def ray_planes(layout: Layout, device="cuda", stream=None) -> torch.Tensor:
+    """(3, H_A, W_A) fp32 UV-ray directions of every atlas texel (for position_mode = POS_RHO)."""
+    out = torch.empty((3, layout.atlas_h, layout.atlas_w), dtype=torch.float32, device=device)
+    _ok(lib().puv_ray_planes(C.byref(layout), _planes(out), _stream(stream)))
+    return out
+
+
+def with_rho(layout: Layout, center) -> Layout:
+    """A copy of `layout` in POS_RHO mode about `center`."""
+    L = Layout.from_buffer_copy(layout)
+    L.position_mode = POS_RHO
+    L.center[:] = [float(x) for x in center]
+    return L
+
+
+def rho_plane_table(atlas: torch.Tensor, rays: torch.Tensor):
+    """Plane table of a POS_RHO atlas: [rho, -, -, planes 3..D-1, ray x, y, z] (entries 1, 2 unused)."""
+    return [atlas[0], atlas[0], atlas[0]] + [atlas[d] for d in range(3, atlas.shape[0])] + [rays[0], rays[1], rays[2]]
 
 
 def pack_atlas(layout: Layout, level_planes, level_occ=None, stream=None):
@@ -348,7 +383,8 @@ class Renderer:
     def backward(self, atlas, occ, dL, grad=None, mask=None, stream=None):
         if grad is None:
             grad = (torch.zeros_like(atlas) if isinstance(atlas, torch.Tensor) else
-                    torch.zeros((len(atlas),) + tuple(atlas[0].shape), dtype=torch.float32, device=self.device))
+                    torch.zeros((self.layout.planes,) + tuple(atlas[0].shape), dtype=torch.float32,
+                                device=self.device))
         render_backward(self.layout, atlas, occ, self.cams, self.opts, dL, mask, self.state, self.arena, grad,
                         stream)
         return grad

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_sizes_match_header():
     assert C.sizeof(puv.Camera) == 16 * 4 + 4 * 4 + 2 * 4 + 4 + 3 * 4
-    assert C.sizeof(puv.Layout) == 5 * 4 + 16 * 5 * 4
+    assert C.sizeof(puv.Layout) == 5 * 4 + 16 * 5 * 4 + 4 + 3 * 4
     assert C.sizeof(puv.RenderOpts) == 16
 
 
@@ -113,3 +113,31 @@ def test_product_path_has_no_oracle_or_cpu_fallback():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in src.replace("oracle's", "").lower() or f.endswith((".cu", ".cuh")), f
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+@pytest.mark.parametrize("S,K", [(1024, 8), (64, 8), (32, 5), (16, 3), (16, 2), (16, 1)])
+def test_paper_layout_matches_oracle(S, K):
+    """puv_layout_paper (recursive right/below rule) vs the oracle's scaled SPEC.md:257 table."""
+    lay = puv.layout_paper(S, K, 3)
+    rows, cols, place, W, H = orc.layout_paper(S, K)
+    assert (lay.atlas_w, lay.atlas_h) == (W, H)
+    for k in range(K):
+        a = lay.level[k]
+        assert (a.rows, a.cols, a.x, a.y, a.rot90ccw) == (rows[k], cols[k], *place[k])
+    assert lay.position_mode == puv.POS_XYZ and lay.planes == 59
+
+
+def test_rho_layout_validation():
+    lay = puv.with_rho(puv.layout_for_levels([(16, 16)], 0), (0.0, 0.0, 1.0))
+    assert lay.position_mode == puv.POS_RHO and list(lay.center) == [0.0, 0.0, 1.0]
+    bad = puv.with_rho(lay, (0, 0, 0))
+    bad.position_mode = 7
+    cams = _cams()
+    assert puv.lib().puv_query_sizes(C.byref(bad), 2, cams, None, C.byref(C.c_size_t()), C.byref(C.c_size_t())) == -2
+    # rho mode: plane entries 1, 2 may be NULL but the 3 ray planes (D..D+2) must be given
+    sb, _ = puv.query_sizes(lay, cams, puv.opts())
+    o = puv.opts()
+    tab = (C.c_void_p * 17)(*([1, 0, 0] + [1] * 11 + [1, 1, 0]))
+    rc = puv.lib().puv_render_views(C.byref(lay), tab, None, 2, cams, C.byref(o), C.c_void_p(1), C.c_void_p(1), sb,
+                                    C.c_void_p(1), 16, None)
+    assert rc == -1 and "plane 16" in puv.last_error()

@@ -253,6 +253,32 @@ def make_scene(cfg: int, views: int | None = None) -> Scene:
     return sc
 
 
+def rho_scene(cfg: int, shapes, sh_degree: int, cams, centre=(0.0, 0.0, 0.0)) -> Scene:
+    """Seeded inputs of the paper-native atlas (NEXT-1): levels of the given
+    (rows, cols) whose plane 0 holds rho (distance along the texel's UV ray about `centre`,
+    PAPER.md:211-215) and planes 1, 2 are unused (zero).  rho = 1 + 0.25 sin(3 a + p) sin(2 b + q)
+    + N(0, 0.03) on the level grid (a = 2 pi c / cols, b = pi r / rows): a smooth closed surface
+    with per-texel jitter, like a fitted shell.  The remaining planes use the shared draws."""
+    rng = np.random.default_rng(np.random.SeedSequence([*SEED_ROOT, cfg]))
+    D = n_planes(sh_degree)
+    levels = []
+    for (rows, cols) in shapes:
+        n = rows * cols
+        p, q = rng.uniform(0, 2 * math.pi, size=2)
+        b, a = np.meshgrid(math.pi * (np.arange(rows) + 0.5) / rows, 2 * math.pi * (np.arange(cols) + 0.5) / cols,
+                           indexing="ij")
+        rho = 1.0 + 0.25 * np.sin(3 * a + p) * np.sin(2 * b + q) + rng.normal(0, 0.03, size=(rows, cols))
+        attrs = _attributes(rng, n, sh_degree)
+        planes = np.zeros((D, rows, cols), np.float32)
+        planes[0] = rho
+        planes[3:] = attrs.T.reshape(D - 3, rows, cols)
+        labels = (rng.random((rows, cols)) < 0.25).astype(np.uint8)
+        levels.append(Level(planes=planes, occ=np.ones((rows, cols), np.uint8), labels=labels))
+    sc = Scene(cfg, sh_degree, levels, list(cams), f"rho atlas {shapes[0]}.. K={len(shapes)}")
+    sc.meta["centre"] = tuple(float(x) for x in centre)
+    return sc
+
+
 def _flow_field(rng):
     """Smooth seeded flow u_a(p) = sin(k_a . p + phi_a)/sqrt(3), |k_a| = 2 rad/m (C4)."""
     k = rng.normal(size=(3, 3))

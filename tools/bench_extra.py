@@ -2,7 +2,11 @@
 
   label: supp. Alg. 1 flow masking on C4 (1,048,576 Gaussians x 55 cameras, 1080p seeded motion masks):
          (Gaussian, camera) tests per second, CUDA events, warm-up 2, 5 timed calls.
+  rho:   the paper-native atlas (NEXT-1): S = 1024, K = 8 pyramid (2,088,960 texels, 1536^2 atlas), SH3,
+         rho positions on UV rays, C3's 64-view 1080p rig; fwd + L2 + bwd views/s, and the same Gaussians
+         rendered from a materialised xyz atlas (the cost of the ray representation).
 """
+import math
 import json
 import os
 import sys
@@ -13,7 +17,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2602_23040_b200 import puv  # noqa: E402
-from synth.scenes import make_scene, motion_masks  # noqa: E402
+from synth.scenes import make_scene, motion_masks, ring, rho_scene  # noqa: E402
 
 
 def bench_label(steps=5, warmup=2):
@@ -48,7 +52,71 @@ def bench_label(steps=5, warmup=2):
             "workload": "C4 atlas 1024^2 SH3, 55 dome cameras 1920x1080, seeded disc motion masks"}
 
 
+def _time_steps(R, planes, occ, targets, steps, warmup):
+    img = torch.empty(R.image_shape, dtype=torch.float32, device=targets.device)
+    dL = torch.empty_like(img)
+    loss = torch.zeros(1, dtype=torch.float64, device=targets.device)
+    grad = torch.zeros((R.layout.planes,) + tuple(occ.shape), dtype=torch.float32, device=targets.device)
+    R.forward(planes, occ, images=img, check=True)
+
+    def step():
+        grad.zero_()
+        puv.render_views(R.layout, planes, occ, R.cams, R.opts, img, R.state, R.arena)
+        puv.l2_loss_grad(img, targets, dL, loss)
+        R.backward(planes, occ, dL, grad=grad)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    puv.profile_read(reset=True)
+    puv.profile_enable(True)
+    l0 = puv.kernel_launches()
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    puv.profile_enable(False)
+    prof = puv.profile_read(reset=True)
+    ms = e0.elapsed_time(e1) / steps
+    return ms, {k: round(v / steps, 3) for k, v in prof["ms"].items()}, (puv.kernel_launches() - l0) // steps
+
+
+def bench_rho(steps=5, warmup=3):
+    dev = torch.device("cuda")
+    S, K, sh = 1024, 8, 3
+    cams = ring(32, 3.5, 1.0, 1920, 1080, 1400.0) + ring(32, 3.5, 2.0, 1920, 1080, 1400.0, offset=math.pi / 32)
+    lay_x = puv.layout_paper(S, K, sh)
+    shapes = [(lay_x.level[k].rows, lay_x.level[k].cols) for k in range(K)]
+    sc = rho_scene(64, shapes, sh, cams)
+    lay = puv.with_rho(lay_x, (0.0, 0.0, 0.0))
+    atlas, occ = puv.pack_atlas(lay, [torch.from_numpy(lv.planes).to(dev) for lv in sc.levels],
+                                [torch.from_numpy(lv.occ).to(dev) for lv in sc.levels])
+    rays = puv.ray_planes(lay)
+    table = puv.rho_plane_table(atlas, rays)
+    cam_arr = puv.cameras(cams)
+    targets = torch.from_numpy(np.stack([sc.target(v) for v in range(len(cams))])).to(dev)
+    R = puv.Renderer(lay, cam_arr, device=dev)
+    ms, stages, launches = _time_steps(R, table, occ, targets, steps, warmup)
+    n_vis = sum(puv.debug_view(lay, cam_arr, R.state, R.arena, v).n_visible for v in range(len(cams)))
+    del R
+    # the same Gaussians from an xyz atlas (positions materialised by the library's own K1 arithmetic:
+    # mu = c + rho ray, computed here with torch fp32 ops, non-fused, only to build the comparison input)
+    xyz = atlas.clone()
+    xyz[0:3] = rays * atlas[0:1]
+    Rx = puv.Renderer(lay_x, cam_arr, device=dev)
+    ms_x, stages_x, _ = _time_steps(Rx, xyz, occ, targets, steps, warmup)
+    n = sum(r * c for r, c in shapes)
+    return {"row": "NEXT-1 paper-native atlas (rho on UV rays, K=8 pyramid)", "metric": "views/s fwd+bwd",
+            "value": len(cams) / (ms / 1e3), "ms_per_step": ms, "stage_ms_per_step": stages,
+            "gpu_launches_per_step": launches, "xyz_atlas_views_per_s": len(cams) / (ms_x / 1e3),
+            "xyz_stage_ms_per_step": stages_x, "gaussians": n, "atlas": [lay.atlas_w, lay.atlas_h],
+            "visible_per_view": n_vis / len(cams),
+            "workload": "S=1024 K=8 rho atlas SH3 (2,088,960 G), C3 64-view ring rig 1920x1080, synthetic shell"}
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["label"]
+    which = sys.argv[1:] or ["label", "rho"]
     for w in which:
-        print(json.dumps({"label": bench_label}[w]()), flush=True)
+        print(json.dumps({"label": bench_label, "rho": bench_rho}[w]()), flush=True)

@@ -158,6 +158,33 @@ puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_
 puv_status puv_l2_loss_grad(int64_t n, const float* images, const float* targets, float* dL_dimages, double* loss,
                             void* stream);
 
+/* The paper's photometric objective (NEXT-4; readings L1-L4 of DESIGN.md §12):
+ *   loss = sum_views (1 - lambda_ssim) mean|I^ - I| + lambda_ssim (1 - mean SSIM(I^, I)),
+ * means over the view's 3 H W entries; SSIM of Wang et al. with an 11 x 11 Gaussian window
+ * (sigma 1.5), C1 = 0.01^2, C2 = 0.03^2, zero-padded windows, per channel; statistics in fp64.
+ * dL_dimages = d loss / d images (sign(0) = 0 for the L1 term), OVERWRITTEN; loss: device double,
+ * OVERWRITTEN.  images/targets/dL_dimages: device, n_views*3*H*W floats (CHW per view).
+ * workspace: device, >= puv_photo_workspace_bytes(W, H, 1) bytes; views are processed in chunks of
+ * as many as the workspace holds (puv_photo_workspace_bytes(W, H, v) for v views per chunk).
+ * lambda_ssim in [0, 1] (0.2 when the caller has no value: L1). */
+size_t puv_photo_workspace_bytes(int32_t width, int32_t height, int32_t views_per_chunk);
+puv_status puv_photo_loss_grad(int32_t n_views, int32_t width, int32_t height, const float* images,
+                               const float* targets, double lambda_ssim, float* dL_dimages, double* loss,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
+/* The paper's regularisers (readings L5-L7 of DESIGN.md §12):
+ *   loss = lambda_scale E_i[max(0, max_a exp(ls_ia) - s_max)]^2 + lambda_opacity E_i alpha_i (1 - alpha_i),
+ * alpha = sigmoid(opacity logit), E_i the mean over occupied texels (atlas_occ != 0, or all if NULL)
+ * that are dynamic (dynamic_mask != 0; all if NULL).  loss: device double, OVERWRITTEN (0 when no
+ * texel is selected).  Gradients are ACCUMULATED (+=) onto atlas_grad planes 3, 4, 5 (the argmax
+ * axis; ties -> lowest) and 10; only those four entries of atlas_planes / atlas_grad are read.
+ * workspace: device, >= puv_reg_workspace_bytes() bytes.  (lambdas 1e-4.) */
+size_t puv_reg_workspace_bytes(void);
+puv_status puv_reg_loss_grad(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                             const uint8_t* dynamic_mask, double lambda_scale, double lambda_opacity, double s_max,
+                             float* const* atlas_grad, double* loss, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 /* Backward of the last puv_render_views with the same layout/cams/opts/state/arena
  * (steps a7-a9).  dL_dimages: device, like images.  dynamic_mask: device
  * H_A*W_A bytes (D_i of PAPER.md:410-414) or NULL.  atlas_grad: host array of D
@@ -214,7 +241,7 @@ puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_c
  * device milliseconds, the kernels launched and the number of timed stage
  * instances; kernel_launches counts every kernel the library launched since it
  * was loaded (profiling on or off).  Stages: */
-#define PUV_NUM_STAGES 9
+#define PUV_NUM_STAGES 10
 enum {
   PUV_STAGE_PROJECT = 0,      /* K1 unpack + EWA projection + SH colour + rect (rows a1, a2) */
   PUV_STAGE_DEPTH_SORT = 1,   /* K3 depth radix sort with culling compaction (row a4, low digit) */
@@ -224,7 +251,8 @@ enum {
   PUV_STAGE_RASTER_BWD = 5,   /* K6 composite backward (row a7) */
   PUV_STAGE_PROJECT_BWD = 6,  /* K7 projection + unpack backward, scatter to texels (rows a8, a9) */
   PUV_STAGE_PACK = 7,         /* K9 pack / unpack */
-  PUV_STAGE_LABEL = 8         /* K11 flow masking (supp. Alg. 1) */
+  PUV_STAGE_LABEL = 8,        /* K11 flow masking (supp. Alg. 1) */
+  PUV_STAGE_OBJECTIVE = 9     /* K12/K13 L1+SSIM photometric loss, regularisers (NEXT-4) */
 };
 typedef struct {
   double ms[PUV_NUM_STAGES];

@@ -472,6 +472,54 @@ puv_status puv_l2_loss_grad(int64_t n, const float* images, const float* targets
   return cuda_check("puv_l2_loss_grad");
 }
 
+size_t puv_photo_workspace_bytes(int32_t width, int32_t height, int32_t views_per_chunk) {
+  if (width < 1 || height < 1 || views_per_chunk < 1) return 0;
+  return (size_t)views_per_chunk * puv::photo_view_bytes(width, height);
+}
+
+puv_status puv_photo_loss_grad(int32_t n_views, int32_t width, int32_t height, const float* images,
+                               const float* targets, double lambda_ssim, float* dL_dimages, double* loss,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_views < 1 || width < 1 || height < 1) return fail(PUV_E_INVALID_ARGUMENT, "bad sizes %d x %d x %d",
+                                                          n_views, width, height);
+  if ((int64_t)width * height > ((int64_t)1 << 28)) return fail(PUV_E_UNSUPPORTED, "image too large");
+  if (!images || !targets || !dL_dimages || !loss || !workspace) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
+  if (!(lambda_ssim >= 0.0 && lambda_ssim <= 1.0)) return fail(PUV_E_INVALID_ARGUMENT, "lambda_ssim outside [0, 1]");
+  const size_t per = puv::photo_view_bytes(width, height);
+  if (workspace_bytes < per)
+    return fail(PUV_E_WORKSPACE_TOO_SMALL, "workspace_bytes %zu < %zu (one view)", workspace_bytes, per);
+  const int chunk = (int)std::min<size_t>((size_t)n_views, workspace_bytes / per);
+  { StageScope sc(PUV_STAGE_OBJECTIVE, (cudaStream_t)stream);
+    puv::launch_photo_loss(n_views, width, height, images, targets, lambda_ssim, dL_dimages, loss, workspace, chunk,
+                           (cudaStream_t)stream); }
+  return cuda_check("puv_photo_loss_grad");
+}
+
+size_t puv_reg_workspace_bytes(void) { return puv::reg_workspace_bytes(); }
+
+puv_status puv_reg_loss_grad(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                             const uint8_t* dynamic_mask, double lambda_scale, double lambda_opacity, double s_max,
+                             float* const* atlas_grad, double* loss, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  if (!atlas_planes || !atlas_grad || !loss || !workspace) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
+  if (workspace_bytes < puv::reg_workspace_bytes())
+    return fail(PUV_E_WORKSPACE_TOO_SMALL, "workspace_bytes %zu < %zu", workspace_bytes, puv::reg_workspace_bytes());
+  PlaneTab P{};
+  GradTab G{};
+  for (int d : {3, 4, 5, 10}) {
+    if (!atlas_planes[d] || !atlas_grad[d]) return fail(PUV_E_INVALID_ARGUMENT, "plane %d is NULL", d);
+    P.p[d] = atlas_planes[d];
+    G.p[d] = atlas_grad[d];
+  }
+  const int64_t N = (int64_t)layout->atlas_w * layout->atlas_h;
+  { StageScope sc(PUV_STAGE_OBJECTIVE, (cudaStream_t)stream);
+    puv::launch_reg_loss(P, atlas_occ, dynamic_mask, N, lambda_scale, lambda_opacity, s_max, G, loss, workspace,
+                         (cudaStream_t)stream); }
+  return cuda_check("puv_reg_loss_grad");
+}
+
 puv_status puv_render_backward(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
                                int32_t n_views, const puv_camera* cams, const puv_render_opts* opts,
                                const float* dL_dimages, const uint8_t* dynamic_mask, void* state, size_t state_bytes,

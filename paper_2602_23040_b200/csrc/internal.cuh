@@ -117,6 +117,12 @@ void launch_unpack(const puv_layout& L, const float* const* atlas_planes, float*
 void launch_contract(int op, const float* in, float* out, int64_t n, cudaStream_t s);
 void launch_label(const Plan& p, const PlaneTab& P, const uint8_t* occ, const CamDev& cam, const uint8_t* mask,
                   uint32_t* sat, int r_max, int first, uint8_t* labels, cudaStream_t s);
+size_t photo_view_bytes(int W, int H);
+void launch_photo_loss(int nviews, int W, int H, const float* img, const float* tgt, double lam, float* dl,
+                       double* loss, void* ws, int chunk, cudaStream_t s);
+size_t reg_workspace_bytes();
+void launch_reg_loss(const PlaneTab& P, const uint8_t* occ, const uint8_t* mask, int64_t N, double lam_s,
+                     double lam_o, double s_max, const GradTab& G, double* loss, void* ws, cudaStream_t s);
 void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaStream_t s);
 
 }  // namespace puv

@@ -63,8 +63,9 @@ class ViewDebug(C.Structure):
                 ("depth_order", C.c_void_p), ("n_examined", C.c_uint64), ("n_composited", C.c_uint64)]
 
 
-NUM_STAGES = 9
-STAGES = ("project", "depth_sort", "bin", "raster_fwd", "loss", "raster_bwd", "project_bwd", "pack", "label")
+NUM_STAGES = 10
+STAGES = ("project", "depth_sort", "bin", "raster_fwd", "loss", "raster_bwd", "project_bwd", "pack", "label",
+          "objective")
 
 
 class Profile(C.Structure):
@@ -101,6 +102,14 @@ def lib():
         L.puv_label_workspace_bytes.restype = C.c_size_t
         L.puv_label_dynamic.argtypes = [P, P, P, S, P, P, S, P, P, C.c_size_t, P]
         L.puv_label_dynamic.restype = C.c_int32
+        L.puv_photo_workspace_bytes.argtypes = [S, S, S]
+        L.puv_photo_workspace_bytes.restype = C.c_size_t
+        L.puv_photo_loss_grad.argtypes = [S, S, S, P, P, C.c_double, P, P, P, C.c_size_t, P]
+        L.puv_photo_loss_grad.restype = C.c_int32
+        L.puv_reg_workspace_bytes.argtypes = []
+        L.puv_reg_workspace_bytes.restype = C.c_size_t
+        L.puv_reg_loss_grad.argtypes = [P, P, P, P, C.c_double, C.c_double, C.c_double, P, P, P, C.c_size_t, P]
+        L.puv_reg_loss_grad.restype = C.c_int32
         L.puv_profile_enable.argtypes = [S]
         L.puv_profile_read.argtypes = [P, S]
         L.puv_profile_enable.restype = C.c_int32
@@ -256,6 +265,37 @@ def render_views(layout, atlas, occ, cams, opts_, images, state, arena, stream=N
 
 def l2_loss_grad(images, targets, dL, loss, stream=None):
     _ok(lib().puv_l2_loss_grad(images.numel(), _ptr(images), _ptr(targets), _ptr(dL), _ptr(loss), _stream(stream)))
+
+
+def photo_workspace_bytes(width: int, height: int, views_per_chunk: int = 1) -> int:
+    return int(lib().puv_photo_workspace_bytes(width, height, views_per_chunk))
+
+
+def photo_loss_grad(images, targets, dL, loss, lambda_ssim=0.2, workspace=None, stream=None):
+    """L1 + SSIM photometric loss (PAPER.md:449-452).  images/targets/dL: (V, 3, H, W) fp32 CUDA;
+    loss: (1,) fp64 CUDA, overwritten.  Returns the workspace (reuse it across calls)."""
+    V, _, H, W = images.shape
+    if workspace is None:
+        workspace = torch.empty(photo_workspace_bytes(W, H, min(V, 8)), dtype=torch.uint8, device=images.device)
+    _ok(lib().puv_photo_loss_grad(V, W, H, _ptr(images), _ptr(targets), float(lambda_ssim), _ptr(dL), _ptr(loss),
+                                  _ptr(workspace), workspace.numel(), _stream(stream)))
+    return workspace
+
+
+def reg_workspace_bytes() -> int:
+    return int(lib().puv_reg_workspace_bytes())
+
+
+def reg_loss_grad(layout, atlas, occ, grad, loss, lambda_scale=1e-4, lambda_opacity=1e-4, s_max=0.05, mask=None,
+                  workspace=None, stream=None):
+    """Scale + opacity regularisers; grad planes ACCUMULATED, loss overwritten."""
+    dev = loss.device
+    if workspace is None:
+        workspace = torch.empty(reg_workspace_bytes(), dtype=torch.uint8, device=dev)
+    _ok(lib().puv_reg_loss_grad(C.byref(layout), _planes(atlas), _ptr(occ), _ptr(mask), float(lambda_scale),
+                                float(lambda_opacity), float(s_max), _planes(grad), _ptr(loss), _ptr(workspace),
+                                workspace.numel(), _stream(stream)))
+    return workspace
 
 
 def render_backward(layout, atlas, occ, cams, opts_, dL, mask, state, arena, grad, stream=None):

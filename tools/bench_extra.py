@@ -5,6 +5,8 @@
   rho:   the paper-native atlas (NEXT-1): S = 1024, K = 8 pyramid (2,088,960 texels, 1536^2 atlas), SH3,
          rho positions on UV rays, C3's 64-view 1080p rig; fwd + L2 + bwd views/s, and the same Gaussians
          rendered from a materialised xyz atlas (the cost of the ray representation).
+  objective: NEXT-4 on C3's shapes: L1+SSIM loss + dL over 64 views of 1920x1080 (vs the L2 harness
+         loss), and the regularisers over the 1024^2 atlas; CUDA events, warm-up 3, 10 timed calls.
 """
 import math
 import json
@@ -116,7 +118,51 @@ def bench_rho(steps=5, warmup=3):
             "workload": "S=1024 K=8 rho atlas SH3 (2,088,960 G), C3 64-view ring rig 1920x1080, synthetic shell"}
 
 
+def _events_ms(fn, steps, warmup):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def bench_objective(steps=10, warmup=3):
+    dev = torch.device("cuda")
+    V, H, W = 64, 1080, 1920
+    g = torch.Generator(device=dev).manual_seed(3)
+    img = torch.rand((V, 3, H, W), device=dev, generator=g) * 0.6 + 0.2
+    tgt = torch.rand((V, 3, H, W), device=dev, generator=g)
+    dL = torch.empty_like(img)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    ws = torch.empty(puv.photo_workspace_bytes(W, H, 8), dtype=torch.uint8, device=dev)
+    l0 = puv.kernel_launches()
+    ms_photo = _events_ms(lambda: puv.photo_loss_grad(img, tgt, dL, loss, 0.2, workspace=ws), steps, warmup)
+    launches = (puv.kernel_launches() - l0) // (steps + warmup)
+    ms_l2 = _events_ms(lambda: puv.l2_loss_grad(img, tgt, dL, loss), steps, warmup)
+    sc = make_scene(3, views=1)
+    lv = sc.levels[0]
+    lay = puv.layout_for_levels([(lv.rows, lv.cols)], 3)
+    atlas = torch.from_numpy(lv.planes).to(dev)
+    occ = torch.from_numpy(lv.occ).to(dev)
+    grad = torch.zeros_like(atlas)
+    rws = torch.empty(puv.reg_workspace_bytes(), dtype=torch.uint8, device=dev)
+    ms_reg = _events_ms(lambda: puv.reg_loss_grad(lay, atlas, occ, grad, loss, 1e-4, 1e-4, 0.05, workspace=rws),
+                        steps, warmup)
+    n = V * 3 * H * W
+    return {"row": "NEXT-4 paper objective (L1 + SSIM, scale/opacity regularisers)", "metric": "views/s (loss + dL)",
+            "value": V / (ms_photo / 1e3), "ms_per_call_64_views": ms_photo, "l2_ms_per_call_64_views": ms_l2,
+            "photo_gpix_ch_per_s": n / (ms_photo / 1e3) / 1e9, "gpu_launches_per_call": launches,
+            "reg_ms_per_call_1M_texels": ms_reg,
+            "workload": "64 views 1920x1080x3 fp32 (C3 image shapes), lambda_ssim 0.2, 8-view chunks; "
+                        "regularisers on C3's 1024^2 SH3 atlas, lambdas 1e-4, s_max 0.05"}
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["label", "rho"]
+    which = sys.argv[1:] or ["label", "rho", "objective"]
     for w in which:
-        print(json.dumps({"label": bench_label, "rho": bench_rho}[w]()), flush=True)
+        print(json.dumps({"label": bench_label, "rho": bench_rho, "objective": bench_objective}[w]()), flush=True)

@@ -73,6 +73,12 @@ def lib():
         L.orc_ray_dirs.argtypes = [C.c_int, P, P, P, C.c_int32, C.c_int32, P, P, P]
         L.orc_positions_from_rho.argtypes = [P, P, P, P, P, C.c_int64, P, P, P]
         L.orc_rho_grad.argtypes = [P, P, P, P, P, P, C.c_int64, P]
+        L.orc_quant_code.restype = C.c_uint32
+        L.orc_quant_code.argtypes = [C.c_float, C.c_float, C.c_float, C.c_int]
+        L.orc_dequant.restype = C.c_float
+        L.orc_dequant.argtypes = [C.c_uint32, C.c_float, C.c_float, C.c_int]
+        L.orc_quant_fit.argtypes = [C.c_int, P, P, C.c_int64, P]
+        L.orc_quantize_plane.argtypes = [P, P, C.c_int64, C.c_float, C.c_float, C.c_int, P, P]
         L.orc_pack.argtypes = [C.c_int, P, P, P, C.c_int, P, P, C.c_int32, C.c_int32, P, P]
         _LIB = L
     return _LIB
@@ -178,6 +184,41 @@ def rho_grad(rays, gxyz):
     lib().orc_rho_grad(_ptr(rays[0]), _ptr(rays[1]), _ptr(rays[2]), _ptr(g[0]), _ptr(g[1]), _ptr(g[2]),
                        out.size, _ptr(out))
     return out
+
+
+def quant_code(x, mn, mx, bits):
+    """LPO fake-quantiser code of one value (DESIGN.md §13 Q1-Q3)."""
+    return int(lib().orc_quant_code(x, mn, mx, bits))
+
+
+def dequant(code, mn, mx, bits):
+    return float(lib().orc_dequant(code, mn, mx, bits))
+
+
+def quant_fit(planes, occ, skip=()):
+    """(D, 2) fp32 per-plane (min, max) over occupied texels; planes in `skip` -> (0, 0)."""
+    planes = np.ascontiguousarray(planes, np.float32)
+    D = planes.shape[0]
+    tab = (C.c_void_p * D)(*[None if d in skip else planes[d].ctypes.data for d in range(D)])
+    o = np.ascontiguousarray(occ, np.uint8) if occ is not None else None
+    spec = np.empty((D, 2), np.float32)
+    lib().orc_quant_fit(D, tab, None if o is None else _ptr(o), planes[0].size, _ptr(spec))
+    return spec
+
+
+def quantize(planes, occ, spec, bits):
+    """Per plane d with bits[d] > 0: codes (uint32) and the fp32 proxy; planes with bits 0 are copied
+    through unchanged with code 0 (the unused planes 1, 2 of rho mode)."""
+    planes = np.ascontiguousarray(planes, np.float32)
+    o = np.ascontiguousarray(occ, np.uint8) if occ is not None else None
+    codes = np.zeros(planes.shape, np.uint32)
+    proxy = planes.copy()
+    for d in range(planes.shape[0]):
+        if bits[d] == 0:
+            continue
+        lib().orc_quantize_plane(_ptr(planes[d]), None if o is None else _ptr(o), planes[d].size,
+                                 float(spec[d, 0]), float(spec[d, 1]), int(bits[d]), _ptr(codes[d]), _ptr(proxy[d]))
+    return codes, proxy
 
 
 def pack(levels, place=None, W=None, H=None):

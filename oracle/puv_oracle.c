@@ -934,3 +934,59 @@ int orc_pack(int K, const int32_t* rows, const int32_t* cols, const int32_t* pla
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-2 low-precision optimisation (LPO): the uniform K-bit fake quantiser  */
+/* of PAPER.md:468-474 / 1295-1311 with SPEC.md:298-313's formulas, in the   */
+/* fp32 contract (readings Q1-Q7):                             */
+/*   L = 2^bits - 1;  t = ((x (-) min) (/) (max (-) min)) (x) L, clamped to   */
+/*   [0, L];  code = round-half-away-from-zero(t);             */
+/*   proxy = min (+) ((code (/) L) (x) (max (-) min));  max == min -> code 0, */
+/*   proxy = min.                                                            */
+
+uint32_t orc_quant_code(float x, float mn, float mx, int bits)
+{
+    if (mx == mn) return 0;
+    const float L = (float)((1u << bits) - 1u);
+    float t = ((x - mn) / (mx - mn)) * L;
+    if (!(t > 0.0f)) t = 0.0f;          /* also maps NaN to 0 */
+    if (t > L) t = L;
+    return (uint32_t)roundf(t);
+}
+
+float orc_dequant(uint32_t code, float mn, float mx, int bits)
+{
+    if (mx == mn) return mn;
+    const float L = (float)((1u << bits) - 1u);
+    return mn + ((float)code / L) * (mx - mn);
+}
+
+/* Per-plane min/max over occupied texels; no occupied texel -> (0, 0). */
+void orc_quant_fit(int D, const float* const* planes, const uint8_t* occ, int64_t n, float* spec /* D x 2 */)
+{
+    for (int d = 0; d < D; ++d) {
+        float mn = 0.0f, mx = 0.0f;
+        int any = 0;
+        if (planes[d])
+            for (int64_t i = 0; i < n; ++i) {
+                if (occ && !occ[i]) continue;
+                const float v = planes[d][i];
+                if (!any || v < mn) mn = v;
+                if (!any || v > mx) mx = v;
+                any = 1;
+            }
+        spec[2 * d] = mn;
+        spec[2 * d + 1] = mx;
+    }
+}
+
+/* Codes (uint32) and proxy of one plane; unoccupied texels: code 0, proxy 0. */
+void orc_quantize_plane(const float* x, const uint8_t* occ, int64_t n, float mn, float mx, int bits, uint32_t* code,
+                        float* proxy)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        if (occ && !occ[i]) { code[i] = 0; proxy[i] = 0.0f; continue; }
+        code[i] = orc_quant_code(x[i], mn, mx, bits);
+        proxy[i] = orc_dequant(code[i], mn, mx, bits);
+    }
+}

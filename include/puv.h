@@ -185,6 +185,28 @@ puv_status puv_reg_loss_grad(const puv_layout* layout, const float* const* atlas
                              float* const* atlas_grad, double* loss, void* workspace, size_t workspace_bytes,
                              void* stream);
 
+/* Low-precision optimisation (LPO, NEXT-2; readings Q1-Q7 of
+ * DESIGN.md §13).  Training renders a uniformly quantised proxy of the fp32 master planes and
+ * passes gradients straight through (STE): call puv_quantize for the proxy, render / backward the
+ * proxy with the usual calls, and accumulate the backward into the MASTER gradient planes.
+ *
+ * puv_quant_fit: per-plane (min, max) over occupied texels -> spec, a device array
+ * of D x 2 floats (OVERWRITTEN; (0, 0) for a plane with no occupied texel and for the unused planes
+ * 1, 2 of PUV_POS_RHO).  Exact (order independent).
+ * puv_quantize: per texel and plane, in the fp32 contract,
+ *   L = 2^bits - 1, t = clamp(((x - min) / (max - min)) * L, 0, L), code = round half away (t),
+ *   proxy = min + (code / L) * (max - min);  max == min -> code 0, proxy = min;
+ * bits = pos_bits for the position planes (0..2, or plane 0 = rho), attr_bits for the others
+ * (16 and 8; each 1..16).  Unoccupied texels: code 0, proxy 0.  codes: NULL, or a
+ * host table of D device pointers to uint8 planes (bits <= 8) / uint16 planes (bits > 8; the two
+ * bytes are the hi/lo 8-bit planes of SPEC.md:313); proxy: NULL or a host table of D device fp32
+ * planes.  Entries for rho mode's planes 1, 2 are ignored (may be NULL). */
+puv_status puv_quant_fit(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                         float* spec, void* stream);
+puv_status puv_quantize(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                        const float* spec, int32_t pos_bits, int32_t attr_bits, void* const* codes,
+                        float* const* proxy, void* stream);
+
 /* Backward of the last puv_render_views with the same layout/cams/opts/state/arena
  * (steps a7-a9).  dL_dimages: device, like images.  dynamic_mask: device
  * H_A*W_A bytes (D_i of PAPER.md:410-414) or NULL.  atlas_grad: host array of D
@@ -241,7 +263,7 @@ puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_c
  * device milliseconds, the kernels launched and the number of timed stage
  * instances; kernel_launches counts every kernel the library launched since it
  * was loaded (profiling on or off).  Stages: */
-#define PUV_NUM_STAGES 10
+#define PUV_NUM_STAGES 11
 enum {
   PUV_STAGE_PROJECT = 0,      /* K1 unpack + EWA projection + SH colour + rect (rows a1, a2) */
   PUV_STAGE_DEPTH_SORT = 1,   /* K3 depth radix sort with culling compaction (row a4, low digit) */
@@ -252,7 +274,8 @@ enum {
   PUV_STAGE_PROJECT_BWD = 6,  /* K7 projection + unpack backward, scatter to texels (rows a8, a9) */
   PUV_STAGE_PACK = 7,         /* K9 pack / unpack */
   PUV_STAGE_LABEL = 8,        /* K11 flow masking (supp. Alg. 1) */
-  PUV_STAGE_OBJECTIVE = 9     /* K12/K13 L1+SSIM photometric loss, regularisers (NEXT-4) */
+  PUV_STAGE_OBJECTIVE = 9,    /* K12/K13 L1+SSIM photometric loss, regularisers (NEXT-4) */
+  PUV_STAGE_QUANT = 10        /* K14 LPO range fit + fake quantiser (NEXT-2) */
 };
 typedef struct {
   double ms[PUV_NUM_STAGES];

@@ -472,6 +472,51 @@ puv_status puv_l2_loss_grad(int64_t n, const float* images, const float* targets
   return cuda_check("puv_l2_loss_grad");
 }
 
+puv_status puv_quant_fit(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                         float* spec, void* stream) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  if (!atlas_planes || !spec) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
+  const bool rho = layout->position_mode == PUV_POS_RHO;
+  PlaneTab P{};
+  for (int d = 0; d < layout->planes; ++d) {
+    if (rho && (d == 1 || d == 2)) continue;
+    if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+    P.p[d] = atlas_planes[d];
+  }
+  { StageScope sc(PUV_STAGE_QUANT, (cudaStream_t)stream);
+    puv::launch_quant_fit(P, layout->planes, atlas_occ, (int64_t)layout->atlas_w * layout->atlas_h, spec,
+                          (cudaStream_t)stream); }
+  return cuda_check("puv_quant_fit");
+}
+
+puv_status puv_quantize(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                        const float* spec, int32_t pos_bits, int32_t attr_bits, void* const* codes,
+                        float* const* proxy, void* stream) {
+  puv_status st = check_layout(layout);
+  if (st) return st;
+  if (!atlas_planes || !spec) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
+  if (pos_bits < 1 || pos_bits > 16 || attr_bits < 1 || attr_bits > 16)
+    return fail(PUV_E_INVALID_ARGUMENT, "bits (%d, %d) outside 1..16", pos_bits, attr_bits);
+  if (!codes && !proxy) return fail(PUV_E_INVALID_ARGUMENT, "codes and proxy are both NULL");
+  const bool rho = layout->position_mode == PUV_POS_RHO;
+  const int D = layout->planes;
+  const float* x[kMaxPlanes] = {};
+  int8_t bits[kMaxPlanes] = {};
+  for (int d = 0; d < D; ++d) {
+    if (rho && (d == 1 || d == 2)) continue;
+    if (!atlas_planes[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
+    if (codes && !codes[d]) return fail(PUV_E_INVALID_ARGUMENT, "code plane %d is NULL", d);
+    if (proxy && !proxy[d]) return fail(PUV_E_INVALID_ARGUMENT, "proxy plane %d is NULL", d);
+    x[d] = atlas_planes[d];
+    bits[d] = (int8_t)((d < 3) ? pos_bits : attr_bits);
+  }
+  { StageScope sc(PUV_STAGE_QUANT, (cudaStream_t)stream);
+    puv::launch_quantize(x, proxy, codes, bits, D, spec, atlas_occ, (int64_t)layout->atlas_w * layout->atlas_h,
+                         (cudaStream_t)stream); }
+  return cuda_check("puv_quantize");
+}
+
 size_t puv_photo_workspace_bytes(int32_t width, int32_t height, int32_t views_per_chunk) {
   if (width < 1 || height < 1 || views_per_chunk < 1) return 0;
   return (size_t)views_per_chunk * puv::photo_view_bytes(width, height);

@@ -123,6 +123,9 @@ void launch_photo_loss(int nviews, int W, int H, const float* img, const float* 
 size_t reg_workspace_bytes();
 void launch_reg_loss(const PlaneTab& P, const uint8_t* occ, const uint8_t* mask, int64_t N, double lam_s,
                      double lam_o, double s_max, const GradTab& G, double* loss, void* ws, cudaStream_t s);
+void launch_quant_fit(const PlaneTab& P, int D, const uint8_t* occ, int64_t N, float* spec, cudaStream_t s);
+void launch_quantize(const float* const* x, float* const* proxy, void* const* code, const int8_t* bits, int D,
+                     const float* spec, const uint8_t* occ, int64_t N, cudaStream_t s);
 void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaStream_t s);
 
 }  // namespace puv

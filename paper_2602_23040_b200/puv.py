@@ -63,9 +63,9 @@ class ViewDebug(C.Structure):
                 ("depth_order", C.c_void_p), ("n_examined", C.c_uint64), ("n_composited", C.c_uint64)]
 
 
-NUM_STAGES = 10
+NUM_STAGES = 11
 STAGES = ("project", "depth_sort", "bin", "raster_fwd", "loss", "raster_bwd", "project_bwd", "pack", "label",
-          "objective")
+          "objective", "quant")
 
 
 class Profile(C.Structure):
@@ -110,6 +110,10 @@ def lib():
         L.puv_reg_workspace_bytes.restype = C.c_size_t
         L.puv_reg_loss_grad.argtypes = [P, P, P, P, C.c_double, C.c_double, C.c_double, P, P, P, C.c_size_t, P]
         L.puv_reg_loss_grad.restype = C.c_int32
+        L.puv_quant_fit.argtypes = [P, P, P, P, P]
+        L.puv_quant_fit.restype = C.c_int32
+        L.puv_quantize.argtypes = [P, P, P, P, S, S, P, P, P]
+        L.puv_quantize.restype = C.c_int32
         L.puv_profile_enable.argtypes = [S]
         L.puv_profile_read.argtypes = [P, S]
         L.puv_profile_enable.restype = C.c_int32
@@ -265,6 +269,39 @@ def render_views(layout, atlas, occ, cams, opts_, images, state, arena, stream=N
 
 def l2_loss_grad(images, targets, dL, loss, stream=None):
     _ok(lib().puv_l2_loss_grad(images.numel(), _ptr(images), _ptr(targets), _ptr(dL), _ptr(loss), _stream(stream)))
+
+
+def quant_fit(layout, atlas, occ, spec=None, stream=None):
+    """LPO: per-plane (min, max) over occupied texels -> (D, 2) fp32 CUDA tensor."""
+    dev = atlas.device if isinstance(atlas, torch.Tensor) else atlas[0].device
+    if spec is None:
+        spec = torch.empty((layout.planes, 2), dtype=torch.float32, device=dev)
+    _ok(lib().puv_quant_fit(C.byref(layout), _planes(atlas), _ptr(occ), _ptr(spec), _stream(stream)))
+    return spec
+
+
+def quantize(layout, atlas, occ, spec, pos_bits=16, attr_bits=8, proxy=None, codes=False, stream=None):
+    """LPO fake quantiser.  Returns (proxy (D, H_A, W_A) fp32 or None, code planes list or None); code
+    planes are uint8 (bits <= 8) or uint16 (bits > 8).  proxy=False skips the proxy."""
+    dev = spec.device
+    shp = (layout.atlas_h, layout.atlas_w)
+    rho = layout.position_mode == POS_RHO
+    if proxy is None:
+        proxy = torch.empty((layout.planes,) + shp, dtype=torch.float32, device=dev)
+        if rho:
+            proxy[1:3] = atlas[1:3] if isinstance(atlas, torch.Tensor) else 0.0
+    ptab = None if proxy is False else _planes(proxy)
+    code_list = None
+    ctab = None
+    if codes:
+        code_list = []
+        for d in range(layout.planes):
+            bits = pos_bits if d < 3 else attr_bits
+            code_list.append(torch.zeros(shp, dtype=torch.uint16 if bits > 8 else torch.uint8, device=dev))
+        ctab = _ptr_table(code_list)
+    _ok(lib().puv_quantize(C.byref(layout), _planes(atlas), _ptr(occ), _ptr(spec), int(pos_bits), int(attr_bits),
+                           ctab, ptab, _stream(stream)))
+    return (None if proxy is False else proxy), code_list
 
 
 def photo_workspace_bytes(width: int, height: int, views_per_chunk: int = 1) -> int:

@@ -5,6 +5,8 @@
   rho:   the paper-native atlas (NEXT-1): S = 1024, K = 8 pyramid (2,088,960 texels, 1536^2 atlas), SH3,
          rho positions on UV rays, C3's 64-view 1080p rig; fwd + L2 + bwd views/s, and the same Gaussians
          rendered from a materialised xyz atlas (the cost of the ray representation).
+  lpo:   NEXT-2 on C3: per step quant_fit + quantize (16-bit xyz, 8-bit rest) + the proxy render fwd + L2 +
+         bwd into the master gradient (STE), views/s vs the plain step; the quantiser's HBM GB/s.
   objective: NEXT-4 on C3's shapes: L1+SSIM loss + dL over 64 views of 1920x1080 (vs the L2 harness
          loss), and the regularisers over the 1024^2 atlas; CUDA events, warm-up 3, 10 timed calls.
 """
@@ -162,7 +164,71 @@ def bench_objective(steps=10, warmup=3):
                         "regularisers on C3's 1024^2 SH3 atlas, lambdas 1e-4, s_max 0.05"}
 
 
+def bench_lpo(steps=5, warmup=3):
+    dev = torch.device("cuda")
+    sc = make_scene(3)
+    lv = sc.levels[0]
+    layout = puv.layout_for_levels([(lv.rows, lv.cols)], 3)
+    atlas = torch.from_numpy(lv.planes).to(dev)
+    occ = torch.from_numpy(lv.occ).to(dev)
+    cams = puv.cameras(sc.cameras)
+    targets = torch.from_numpy(np.stack([sc.target(v) for v in range(len(sc.cameras))])).to(dev)
+    R = puv.Renderer(layout, cams, device=dev)
+    spec = puv.quant_fit(layout, atlas, occ)
+    proxy, _ = puv.quantize(layout, atlas, occ, spec)
+    img = torch.empty(R.image_shape, dtype=torch.float32, device=dev)
+    dL = torch.empty_like(img)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    grad = torch.zeros_like(atlas)
+    R.forward(proxy, occ, images=img, check=True)
+
+    def step(lpo):
+        grad.zero_()
+        src = atlas
+        if lpo:
+            puv.quant_fit(layout, atlas, occ, spec=spec)
+            puv.quantize(layout, atlas, occ, spec, proxy=proxy)
+            src = proxy
+        puv.render_views(layout, src, occ, R.cams, R.opts, img, R.state, R.arena)
+        puv.l2_loss_grad(img, targets, dL, loss)
+        R.backward(src, occ, dL, grad=grad)
+
+    out = {}
+    for lpo in (True, False):
+        for _ in range(warmup):
+            step(lpo)
+        torch.cuda.synchronize()
+        puv.profile_read(reset=True)
+        puv.profile_enable(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step(lpo)
+        e1.record()
+        torch.cuda.synchronize()
+        puv.profile_enable(False)
+        prof = puv.profile_read(reset=True)
+        out[lpo] = (e0.elapsed_time(e1) / steps, {k: round(v / steps, 3) for k, v in prof["ms"].items()})
+    # the quantiser alone: reads D fp32 planes, writes D fp32 proxy planes (+ occ)
+    qms = _events_ms(lambda: puv.quantize(layout, atlas, occ, spec, proxy=proxy), 20, 3)
+    n = lv.rows * lv.cols
+    qbytes = n * (layout.planes * 8 + 1)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    ms_l, st_l = out[True]
+    ms_p, _ = out[False]
+    return {"row": "NEXT-2 LPO (16-bit xyz / 8-bit attributes fake quantiser, STE)", "metric": "views/s fwd+bwd",
+            "value": len(sc.cameras) / (ms_l / 1e3), "ms_per_step": ms_l, "plain_views_per_s":
+            len(sc.cameras) / (ms_p / 1e3), "stage_ms_per_step": st_l, "quantize_ms": qms,
+            "quantize_roofline": {"bound": "hbm", "achieved": qbytes / (qms / 1e3) / 1e9, "peak": hbm,
+                                  "unit": "GB/s", "frac": qbytes / (qms / 1e3) / 1e9 / hbm,
+                                  "bytes_per_launch": qbytes},
+            "workload": "C3 1024^2 SH3 atlas, 64 views 1920x1080, range refit every step"}
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["label", "rho", "objective"]
+    which = sys.argv[1:] or ["label", "rho", "objective", "lpo"]
+    rows = {"label": bench_label, "rho": bench_rho, "objective": bench_objective, "lpo": bench_lpo}
     for w in which:
-        print(json.dumps({"label": bench_label, "rho": bench_rho, "objective": bench_objective}[w]()), flush=True)
+        print(json.dumps(rows[w]()), flush=True)

@@ -582,9 +582,10 @@ puv_status puv_render_backward(const puv_layout* layout, const float* const* atl
   const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
   cudaStream_t s = (cudaStream_t)stream;
   const Plan& p = c.plan;
-  for (int v = 0; v < n_views; ++v)
+  // all views in one launch (grid = tiles x views): no per-view tail; the background enters
+  // through the forward's full colour C
   { StageScope sc(PUV_STAGE_RASTER_BWD, s);
-    launch_raster_bwd(p, c.views, (const uint32_t*)arena, dL_dimages + (size_t)v * 3 * p.HW, v, bg, s); }
+    launch_raster_bwd(p, c.views, (const uint32_t*)arena, dL_dimages, n_views, s); }
   for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
     CamBatch cb;
     cb.v0 = v0;

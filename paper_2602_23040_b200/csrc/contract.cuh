@@ -24,9 +24,9 @@ constexpr float kLn2Lo = 1.42860677e-6f;
 constexpr float kLog2e = 1.44269504f;
 
 // exp_c (R13): Cody-Waite reduction by ln2 (hi/lo) + degree-7 Taylor, Horner with fma.
-PUV_DEV float exp_c(float x) {
-  if (x >= 88.0f) return __int_as_float(0x7f800000);
-  if (x <= -87.0f) return 0.0f;
+// exp_c_core is exp_c without the range clamps, for callers whose argument is known to lie in (-87, 88) (the
+// compositing range: power in [t_g, 0] with t_g = -log_c(255 o) >= -5.55): bit-identical there.
+PUV_DEV float exp_c_core(float x) {
   const float k = rintf(mul(x, kLog2e));
   float r = fma_(-k, kLn2Hi, x);
   r = fma_(-k, kLn2Lo, r);
@@ -40,6 +40,12 @@ PUV_DEV float exp_c(float x) {
   p = fma_(p, r, 1.0f);
   const float two_k = __int_as_float(((int)k + 127) << 23);
   return mul(p, two_k);
+}
+
+PUV_DEV float exp_c(float x) {
+  if (x >= 88.0f) return __int_as_float(0x7f800000);
+  if (x <= -87.0f) return 0.0f;
+  return exp_c_core(x);
 }
 
 // log_c (R13): m in [sqrt(1/2), sqrt(2)], atanh series in s = f/(2+f).
@@ -69,32 +75,51 @@ PUV_DEV float pair_power(float mx, float my, float ha, float nb, float hc, float
   return fma_(dx, u, mul(mul(hc, dy), dy));
 }
 
-// ---- fp64 exp for the value path (not part of the contract) ----------------------------------
-// exp(x) = 2^m * 2^(j/64) * e^r,  k = rint(64 x / ln2) = 64 m + j,  |r| <= ln2/128,
-// e^r by its degree-5 Taylor polynomial (truncation < 4e-17).  `tab` = 2^(j/64), j < 64,
-// staged in shared memory by the caller (exp64_table_fill).  Valid for x in [-700, 0].
+// ---- fp64 value path helpers (not part of the contract) ---------------------------------------
+// exp(x) = 2^m * 2^(j/64) * e^r,  k = rint(64 x / ln2) = 64 m + j,  r = x - k ln2/64 (one fma:
+// the rounding of ln2/64 costs |k| * 1.2e-18, < 1e-13 over the valid range), |r| <= ln2/128,
+// e^r by its degree-4 Taylor polynomial (truncation < 4e-14).  Measured max relative error vs
+// libm over [-700, 0]: 1.2e-13 -- far below what the gradient tolerance needs.
+// `tab` = 2^(j/64), j < 64, staged in shared memory by the caller (exp64_table_fill).
+// Valid for x in [-700, 1]; for far-out x (inactive pixels of the branch-free backward) the
+// result is garbage but finite-or-inf, and the callers select it away.
 PUV_DEV void exp64_table_fill(double* tab) {
   for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = exp2((double)j / 64.0);
 }
 
 PUV_DEV double exp64(double x, const double* tab) {
   constexpr double kInvL = 92.33248261689366;            // 64 / ln 2
-  constexpr double kLhi = 0.010830424696223417;          // ln2/64 high part (trailing bits zero)
-  constexpr double kLlo = 2.572804622327669e-14;         // ln2/64 - kLhi
+  constexpr double kL = 0.010830424696249145;            // ln 2 / 64
   constexpr double kShift = 6755399441055744.0;          // 1.5 * 2^52: rint by addition
   const double t = fma(x, kInvL, kShift);
   const int k = (int)__double2loint(t);                  // low word = rint(64 x / ln2) (two's complement)
-  const double kd = t - kShift;
-  double r = fma(-kd, kLhi, x);
-  r = fma(-kd, kLlo, r);
-  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  p = fma(r, p, 1.0 / 6.0);
+  const double r = fma(-(t - kShift), kL, x);
+  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
   p = fma(r, p, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);
   const double v = tab[k & 63] * p;
-  const int m = k >> 6;                                  // arithmetic shift: floor(k / 64)
-  return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
+  return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+}
+
+// Gaussian exponent in fp64 from the pixel offset (dx, dy) = mean - pixel; also returns the
+// second-order monomials (shared by K5 and K6 so both evaluate the same rounded value).
+PUV_DEV double power64(double ha, double nb, double hc, double dx, double dy, double& dxx, double& dxy,
+                       double& dyy) {
+  dxx = dx * dx;
+  dxy = dx * dy;
+  dyy = dy * dy;
+  return fma(ha, dxx, fma(nb, dxy, hc * dyy));
+}
+
+// 1/y for y in [0.01, 1]: MUFU fp64 reciprocal estimate + two Newton steps (~1 ulp)
+PUV_DEV double rcp64(double y) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  double e = fma(-y, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-y, r, 1.0);
+  return fma(r, e, r);
 }
 
 }  // namespace puv

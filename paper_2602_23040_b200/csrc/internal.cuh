@@ -106,8 +106,8 @@ void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cud
 void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
 void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* image, int view,
                        const float bg[3], cudaStream_t s);
-void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimage, int view,
-                       const float bg[3], cudaStream_t s);
+void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int n_views,
+                       cudaStream_t s);
 void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const uint8_t* mask,
                         const CamBatch& cb, const GradTab& G, cudaStream_t s);
 void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s);

@@ -44,15 +44,20 @@ __global__ void __launch_bounds__(128) k_project_bwd(PlaneTab P, PosMode pm, con
   for (int i = 0; i < cb.n; ++i) {
     const size_t o = (size_t)(cb.v0 + i) * N + g;
     if (v.depth[o] == kInvisible) continue;
+    // K6's raw moments (Mx, My, Mxx, Mxy, Myy, dL/do, dL/drgb): see k_raster_bwd.cu
     const double* g2 = v.grad2d + 9 * o;
-    const double dmx = g2[0], dmy = g2[1], dha = g2[2], dnb = g2[3], dhc = g2[4], dO = g2[5];
+    const double Mx = g2[0], My = g2[1], Mxx = g2[2], Mxy = g2[3], Myy = g2[4], dO = g2[5];
     const double dr = g2[6], dg = g2[7], db_ = g2[8];
-    if (dmx == 0 && dmy == 0 && dha == 0 && dnb == 0 && dhc == 0 && dO == 0 && dr == 0 && dg == 0 && db_ == 0)
+    if (Mx == 0 && My == 0 && Mxx == 0 && Mxy == 0 && Myy == 0 && dO == 0 && dr == 0 && dg == 0 && db_ == 0)
       continue;
     const CamDev& c = cb.c[i];
     const CamPoint cp = cam_point(c, fmx, fmy, fmz);  // fp32 contract: the same J-clamp decisions as K1
     const Proj64 p = project64(c, mux, muy, muz, u, cp.clx, cp.cly);
     const double a = p.a, b = p.b, cc = p.c, id2 = 1.0 / (p.det * p.det);
+    // power = ha dx^2 + nb dx dy + hc dy^2 with (ha, nb, hc) = (-c/2, b, -a/2) / det, alpha = o e^power
+    const double idet = 1.0 / p.det, ha = -0.5 * cc * idet, nb = b * idet, hc = -0.5 * a * idet;
+    const double dmx = u.o * (2.0 * ha * Mx + nb * My), dmy = u.o * (nb * Mx + 2.0 * hc * My);
+    const double dha = u.o * Mxx, dnb = u.o * Mxy, dhc = u.o * Myy;
     // conic (ha, nb, hc) = (-c/2, b, -a/2) / det
     const double da = (dha * 0.5 * cc * cc - dnb * b * cc + dhc * 0.5 * b * b) * id2;
     const double db = (-dha * b * cc + dnb * (a * cc + b * b) - dhc * a * b) * id2;

@@ -1,21 +1,24 @@
 // K6 k_raster_bwd — per-tile gradient of the front-to-back composite (row a7).
 //
-// One 128-thread block (4 warps) per 16x16 tile; warp w owns the 8x8 pixel
-// quadrant (8(w&1), 8(w>>1)); lane l owns column l & 7 and rows (l >> 3) + 4k,
-// k < PPT = 2.  Every decision (skip test R1, alpha cap, composited set R14) is
-// replayed with the fp32 contract exactly as K5 took it; every VALUE is fp64
-// (DESIGN.md §5).  Single pass in front-to-back order, using the pixel's full
-// colour C from K5:
-//   T_k = prod_{i<k} (1 - a_i),   P_k = sum_{i<=k} c_i a_i T_i,   S_k = C - P_k
-//   dL/dc_k = a_k T_k dL/dC
-//   dL/da_k = sum_ch dL/dC (T_k c_k - S_k / (1 - a_k))
-//   uncapped: dL/do = G dL/da, dL/dpower = o G dL/da -> (mx, my, ha, nb, hc)
-// The per-pixel body is branch-free (inactive pixels get a = 0 and masked
-// terms), so the pixels' fp64 chains interleave (ncu: the branchy version was
-// bound by fixed-latency "wait" stalls).  A thread sums the 9 values of an
-// entry over its pixels; the warp sums them with a transposing butterfly
-// (8 values in 9 double shuffles, the 9th in 5) and 9 lanes issue one fp64
-// atomic each into the (view, Gaussian) gradient slot.
+// One 128-thread block (4 warps) per (16x16 tile, view) — all views of a call in one launch;
+// warp w owns the 8x8 pixel quadrant (8(w&1), 8(w>>1)); lane l owns column l & 7 and rows
+// (l >> 3) + 4k, k < PPT = 2.  Every decision (skip test R1, alpha cap, composited set R14) is
+// replayed with the fp32 contract exactly as K5 took it; every VALUE is fp64.
+// Single pass in front-to-back order, using the pixel's full colour C from K5.  With dC = dL/dC
+// (3 channels) only the scalar projections of the colours are needed:
+//   cd_k = dC . c_k,   Sd_k = dC . (C - P_k) = dC . C - sum_{i<=k} cd_i a_i T_i
+//   dL/dc_k = a_k T_k dC,   dL/da_k = cd_k T_k - Sd_k / (1 - a_k)
+//   uncapped: dL/do = G dL/da, dL/dpower = o G dL/da
+// and, with power = ha dx^2 + nb dx dy + hc dy^2 ((dx, dy) = mean - pixel), the mean and conic
+// gradients are o-scaled moments of GdL = G dL/da over the pixels:
+//   dL/dmx = o (2 ha Mx + nb My), dL/dmy = o (nb Mx + 2 hc My), dL/d(ha, nb, hc) = o (Mxx, Mxy, Myy)
+//   Mx = sum GdL dx, My = sum GdL dy, Mxx = sum GdL dx^2, Mxy = sum GdL dx dy, Myy = sum GdL dy^2.
+// K6 accumulates the raw moments (Mx, My, Mxx, Mxy, Myy, sum GdL, dL/dc) per (view, Gaussian);
+// K7 applies the (linear) o-scaling and the conic mixing once per (view, Gaussian).
+// The per-pixel body is branch-free (inactive pixels get a = 0 and masked terms), so the
+// pixels' fp64 chains interleave.  A thread sums the 9 moments of an entry over its pixels; the
+// warp sums them through a shared-memory transpose (warp_sum9) and 9 lanes issue one fp64 atomic
+// each into the (view, Gaussian) slot.
 #include "contract.cuh"
 #include "internal.cuh"
 
@@ -25,47 +28,46 @@ constexpr int kBwdPPT = 2;                                 // pixels per thread
 constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128
 constexpr int kBwdBatch = 128;                             // entries staged per batch
 
-// Sum v[0..7] across the warp (lane l ends with the total of value (l >> 2) & 7) and v8 (all lanes).
-__device__ __forceinline__ double warp_reduce9(double (&x)[8], double& v8) {
-  const int lane = threadIdx.x & 31;
+constexpr int kRedStride = 9;   // doubles per lane in the per-warp transpose buffer
+
+// Sum the 9 per-lane values x[0..8] over the warp through shared memory: every lane stores its 9
+// values, lanes 3v, 3v+1, 3v+2 (v < 9) each sum value v over a third of the lanes (11/11/10),
+// and two shuffles fold the thirds into lane 3v.  About 40 instructions per entry, against ~90
+// for a select-based transposing shuffle butterfly.  `buf` is the warp's 32 x 9 slice.
+__device__ __forceinline__ double warp_sum9(const double (&x)[9], double* buf, int lane) {
 #pragma unroll
-  for (int level = 0; level < 3; ++level) {
-    const int half = 4 >> level;
-    const int off = 16 >> level;
-    const bool upper = (lane & off) != 0;
+  for (int k = 0; k < 9; ++k) buf[lane * kRedStride + k] = x[k];
+  __syncwarp();
+  const int v = lane / 3, part = lane - 3 * v;
+  double s0 = 0.0, s1 = 0.0;
+  if (lane < 27) {
+    const int l0 = 11 * part, n = part == 2 ? 10 : 11;
+    const double* col = buf + l0 * kRedStride + v;
 #pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = upper ? x[i] : x[i + half];
-      const double keep = upper ? x[i + half] : x[i];
-      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    for (int i = 0; i < 10; i += 2) {
+      s0 += col[i * kRedStride];
+      s1 += col[(i + 1) * kRedStride];
     }
+    if (n == 11) s0 += col[10 * kRedStride];
   }
-  double s = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 2);
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, off);
-  return s;
+  __syncwarp();
+  double s = s0 + s1;
+  const double p1 = __shfl_down_sync(0xffffffffu, s, 1);
+  const double p2 = __shfl_down_sync(0xffffffffu, s, 2);
+  return s + p1 + p2;   // valid in lanes 3v, v < 9
 }
 
-// 1/y for y in [0.01, 1]: fp32 reciprocal estimate + two Newton steps in fp64 (~1 ulp)
-__device__ __forceinline__ double rcp64(double y) {
-  double r = (double)__frcp_rn((float)y);
-  double e = fma(-y, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-y, r, 1.0);
-  return fma(r, e, r);
-}
-
-__global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int view,
-                                                           int N, int W, int H, int gx, int ntiles,
-                                                           const float* __restrict__ dL_dimage) {
+__global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int N,
+                                                           int W, int H, int gx, int ntiles,
+                                                           const float* __restrict__ dL_dimages) {
   __shared__ float4 sA[kBwdBatch], sB[kBwdBatch];
   __shared__ double2 sD[5][kBwdBatch];
   __shared__ uint32_t sG[kBwdBatch];
   __shared__ uint32_t smax[kBwdThreads / 32];
+  __shared__ double sRed[kBwdThreads / 32][32 * kRedStride];
   __shared__ double sExp[64];
   exp64_table_fill(sExp);
-  const int tile = blockIdx.x;
+  const int tile = blockIdx.x, view = blockIdx.y;
   const int tx = tile % gx, ty = tile / gx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const ViewHdr& hdr = v.hdr[view];
@@ -76,10 +78,11 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   double* g2 = v.grad2d + (size_t)view * N * 9;
   const size_t HW = (size_t)W * H;
+  const float* dL_dimage = dL_dimages + (size_t)view * 3 * HW;
   float fi[kBwdPPT], fj[kBwdPPT];
+  double di[kBwdPPT], dj[kBwdPPT];
   uint32_t last[kBwdPPT];
-  float dC[kBwdPPT][3];
-  double S[kBwdPPT][3], T[kBwdPPT];
+  double dC[kBwdPPT][3], Sd[kBwdPPT], T[kBwdPPT];
   uint32_t tlast = 0;
 #pragma unroll
   for (int k = 0; k < kBwdPPT; ++k) {
@@ -88,10 +91,13 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
     const int py = ty * kTile + (warp >> 1) * 8 + (lane >> 3) + 4 * k;
     fi[k] = (float)px;
     fj[k] = (float)py;
+    di[k] = px;
+    dj[k] = py;
     last[k] = 0;
     T[k] = 1.0;
+    Sd[k] = 0.0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { dC[k][c] = 0.f; S[k][c] = 0.0; }
+    for (int c = 0; c < 3; ++c) dC[k][c] = 0.0;
     if (px < W && py < H) {
       const size_t p = (size_t)py * W + px;
       last[k] = v.ncontrib[(size_t)view * HW + p];
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         dC[k][c] = dL_dimage[c * HW + p];
-        S[k][c] = cf[c];           // S starts at the full colour C; S_k = C - P_k
+        Sd[k] = fma(dC[k][c], cf[c], Sd[k]);   // Sd starts at dC . C (the full colour)
       }
     }
     tlast = max(tlast, last[k]);
@@ -127,60 +133,61 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
       const uint32_t e = lo + j;
       if (e >= wlast) break;  // warp-uniform: no pixel of this warp reaches entry e
       const float4 A = sA[j], B = sB[j];
-      // decisions (fp32 contract), per pixel
+      // decisions (fp32 contract), per pixel.  The cap needs o (x) exp_c(power) >= 0.99 with
+      // power <= 0, where exp_c <= 1 (its last Horner step is 1 + p r with r <= 0, or 2^k <= 1/2),
+      // so an entry with o < 0.99 is never capped: the exp_c replay runs only for the (rare)
+      // entries with o >= 0.99 (warp-uniform branch).
+      const bool may_cap = !(B.z < 0.99f);
       bool act[kBwdPPT], cap[kBwdPPT];
       bool any = false;
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
         const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
         act[k] = e < last[k] && !(power > 0.0f || power < B.y);
-        cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
+        cap[k] = false;
+        if (may_cap) cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
         any |= act[k];
       }
       if (!__any_sync(0xffffffffu, any)) continue;
       const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
-      const double d4x = sD[4][j].x;
-      double gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      double gb = 0.0;
+      const double cb = sD[4][j].x;
+      const double o = d2.y;
+      double gv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // Mx, My, Mxx, Mxy, Myy, sum GdL, colour r, g, b
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const double dx = d0.x - (double)fi[k], dy = d0.y - (double)fj[k];
-        const double pw = fmax(fma(d1.x * dx, dx, fma(d1.y * dx, dy, d2.x * dy * dy)), -700.0);
-        const double G = exp64(fmin(pw, 0.0), sExp);
-        const double a = act[k] ? (cap[k] ? 0.99 : d2.y * G) : 0.0;
+        const double dx = d0.x - di[k], dy = d0.y - dj[k];
+        double dxx, dxy, dyy;
+        const double pw = power64(d1.x, d1.y, d2.x, dx, dy, dxx, dxy, dyy);
+        const double G = exp64(pw, sExp);
+        const double a = act[k] ? (cap[k] ? 0.99 : o * G) : 0.0;
         const double aT = a * T[k];
-        S[k][0] = fma(-d3.x, aT, S[k][0]);
-        S[k][1] = fma(-d3.y, aT, S[k][1]);
-        S[k][2] = fma(-d4x, aT, S[k][2]);
-        const double iom = rcp64(1.0 - a);
-        const double c0 = dC[k][0], c1 = dC[k][1], c2 = dC[k][2];
-        const double dLda = c0 * (T[k] * d3.x - S[k][0] * iom) + c1 * (T[k] * d3.y - S[k][1] * iom) +
-                            c2 * (T[k] * d4x - S[k][2] * iom);
-        gv[6] = fma(aT, c0, gv[6]);
-        gv[7] = fma(aT, c1, gv[7]);
-        gb = fma(aT, c2, gb);
+        const double cd = fma(dC[k][0], d3.x, fma(dC[k][1], d3.y, dC[k][2] * cb));
+        Sd[k] = fma(-cd, aT, Sd[k]);
+        const double dLda = fma(cd, T[k], -Sd[k] * rcp64(1.0 - a));
+        gv[6] = fma(aT, dC[k][0], gv[6]);
+        gv[7] = fma(aT, dC[k][1], gv[7]);
+        gv[8] = fma(aT, dC[k][2], gv[8]);
         const double GdL = (act[k] && !cap[k]) ? G * dLda : 0.0;
-        const double dP = d2.y * GdL;                        // d alpha / d power = o G
-        gv[5] += GdL;                                        // d alpha / d o = G
-        gv[2] = fma(dx * dx, dP, gv[2]);
-        gv[3] = fma(dx * dy, dP, gv[3]);
-        gv[4] = fma(dy * dy, dP, gv[4]);
-        gv[0] = fma(2.0 * d1.x * dx + d1.y * dy, dP, gv[0]);
-        gv[1] = fma(d1.y * dx + 2.0 * d2.x * dy, dP, gv[1]);
+        gv[5] += GdL;
+        gv[0] = fma(GdL, dx, gv[0]);
+        gv[1] = fma(GdL, dy, gv[1]);
+        gv[2] = fma(GdL, dxx, gv[2]);
+        gv[3] = fma(GdL, dxy, gv[3]);
+        gv[4] = fma(GdL, dyy, gv[4]);
         T[k] -= aT;                                          // T_{k+1} = T_k (1 - a_k)
       }
-      const double s = warp_reduce9(gv, gb);
-      double* dst = g2 + 9 * (size_t)sG[j];
-      if ((lane & 3) == 0) atomicAdd(dst + (lane >> 2), s);
-      if (lane == 1) atomicAdd(dst + 8, gb);
+      // raw moments into the (view, Gaussian) slot; K7 turns them into dL/d(mx, my, ha, nb, hc)
+      const double s = warp_sum9(gv, sRed[warp], lane);
+      if (lane < 27 && lane % 3 == 0) atomicAdd(g2 + 9 * (size_t)sG[j] + lane / 3, s);
     }
   }
 }
 
-void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimage, int view,
-                       const float bg[3], cudaStream_t s) {
-  (void)bg;  // the background enters through the forward's full colour C
-  k_raster_bwd<<<p.ntiles, kBwdThreads, 0, s>>>(arena, v, view, p.N, p.W, p.H, p.gx, p.ntiles, dL_dimage);
+void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int n_views,
+                       cudaStream_t s) {
+  if (n_views <= 0 || p.ntiles <= 0) return;
+  const dim3 grid(p.ntiles, n_views);
+  k_raster_bwd<<<grid, kBwdThreads, 0, s>>>(arena, v, p.N, p.W, p.H, p.gx, p.ntiles, dL_dimages);
   count_launches(1);
 }
 

@@ -189,6 +189,35 @@ def test_edge_ragged_multiview_empty_views_bg_mask():
     assert np.all(grad[:, mask == 0] == 0)
 
 
+def test_high_opacity_alpha_cap_parity():
+    """Opacity logits ~ N(4, 2): a third of the Gaussians have o >= 0.99, so the alpha cap (R9) is
+    active on many pairs (zero gradient through o and the conic there, R10), mixed with uncapped
+    pairs of the same Gaussians; 2 views, ragged 120x90 image, SH degree 1."""
+    rng = np.random.default_rng(11)
+    n = 40 * 30
+    mu = rng.uniform(-1, 1, (n, 3))
+    sh = np.concatenate([rng.random((n, 3)), rng.normal(0, 0.1, (n, 9))], axis=1)
+    cams = [look_at((3.0, 0.3, 0.8), (0, 0, 0), 120, 90, 110.0), look_at((-0.5, 3.0, 1.2), (0, 0, 0), 120, 90, 110.0)]
+    sc = tiny_scene(mu, [-2.4] * 3, [1, 0, 0, 0], rng.normal(4.0, 2.0, n), sh, cams[0], 1)
+    lv = sc.levels[0]
+    lv.planes[3:6] = rng.normal(-2.4, 0.3, (3, 1, n)).astype(np.float32)
+    lv.planes[6:10] = rng.normal(size=(4, 1, n)).astype(np.float32)
+    sc.levels = [Level(planes=np.ascontiguousarray(lv.planes.reshape(-1, 40, 30)),
+                       occ=np.ascontiguousarray(lv.occ.reshape(40, 30)),
+                       labels=np.ascontiguousarray(lv.labels.reshape(40, 30)))]
+    sc.cameras = cams
+    sc.cfg = 98
+    views = [0, 1]
+    planes, occ, _ = oracle_scene(sc)
+    o = 1.0 / (1.0 + np.exp(-planes[10].astype(np.float64)))
+    assert (o >= 0.99).mean() > 0.2
+    _, dls = _oracle_dls(sc, planes, occ, views)
+    g, img, loss, grad = _run(sc, views, dls=dls)
+    for vi in views:
+        _parity_view(sc, g, planes, occ, vi, vi, img[vi])
+    _grad_check(sc, planes, occ, views, dls, grad)
+
+
 def test_arena_overflow_flag_and_retry():
     sc = make_scene(1)
     g = gpu_scene(sc, [0], arena_bytes=4096)

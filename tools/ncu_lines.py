@@ -4,6 +4,14 @@ import csv
 import sys
 from collections import defaultdict
 
+
+def num(x):
+    try:
+        return float(x)
+    except ValueError:
+        return 0.0
+
+
 rows = list(csv.reader(open(sys.argv[1])))
 want = sys.argv[2] if len(sys.argv) > 2 else ""
 cur_file, cur_fn, hdr = None, None, None
@@ -32,9 +40,9 @@ for r in rows:
         continue
     key = (cur_file, r[0])
     a = agg[key]
-    a[0] += float(r[ie] or 0)
-    a[1] += float(r[te] or 0)
-    a[2] += float(r[sm] or 0)
+    a[0] += num(r[ie])
+    a[1] += num(r[te])
+    a[2] += num(r[sm])
     a[3] = r[1][:90]
 tot_i = sum(a[0] for a in agg.values()) or 1
 tot_s = sum(a[2] for a in agg.values()) or 1

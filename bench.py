@@ -170,10 +170,10 @@ def stage_work(stage, c, D):
         return "hbm", 4 * N + 4 * nv
     if stage == "bin":              # read rank rects, write every key once, ranges
         return "hbm", 8 * nv + 4 * K + 8 * c["ntiles"]
-    if stage == "raster_fwd":       # fp64 lane-ops of the value path: 24 per composited pair
-        return "alu_fp64", 24 * P
-    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 58
-        return "alu_fp64", 58 * P
+    if stage == "raster_fwd":       # fp64 lane-ops of the value path: 22 per composited pair
+        return "alu_fp64", 22 * P
+    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 40
+        return "alu_fp64", 40 * P
     if stage == "project_bwd":      # read 2D grads + params, RMW texel grads
         return "hbm", 72 * nv + (D * 4 * 3 * N) / c["views"]
     if stage == "loss":

@@ -146,9 +146,12 @@ puv_status puv_query_sizes(const puv_layout* layout, int32_t n_views, const puv_
  * atlas_planes: host array of D device pointers; atlas_occ: device H_A*W_A bytes
  * or NULL (all occupied).  cams: host array of n_views.  images: device,
  * n_views*3*H*W floats (all views must share W, H).  state: device, >= state_bytes.
- * arena: device, arena_bytes (tile lists, 4 bytes per key).  If the keys do
- * not fit, the overflow flag is set on device, the affected views render
- * nothing, and puv_check_overflow reports the size needed. */
+ * arena: device, arena_bytes.  Per view it holds the K tile-list keys (4 bytes
+ * each) followed by the K1 keys of the level-1 super-tile pass of the binning
+ * (4x4-tile super-tiles, K1 = sum over visible Gaussians of the super-tile
+ * rect areas, ~K/10 at C3).  If a view does not fit, the
+ * overflow flag is set on device, the affected views render nothing, and
+ * puv_check_overflow reports the size needed (4 (K + K1) bytes summed over views). */
 puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
                             int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, float* images,
                             void* state, size_t state_bytes, void* arena, size_t arena_bytes, void* stream);

@@ -217,6 +217,7 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.bsum = stake(4 * (N / 2048 + 2));
   p.cnt = stake(4 * (size_t)kNbMax * p.ntiles);
   p.bstart = stake(4 * (size_t)(kNbMax + 1));
+  p.bin2 = stake(bin_scratch_bytes(N, p.ntiles));
   p.nscratch = n_views < kBinStreams ? n_views : kBinStreams;
   p.scratch_stride = soff;
   p.scratch0 = take(soff * p.nscratch);

@@ -64,7 +64,7 @@ struct Plan {
   size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull;
   // scratch shared by all views (reused in stream order)
   // (offsets relative to one scratch block; block i starts at scratch0 + i * scratch_stride)
-  size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt, bstart;
+  size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt, bstart, bin2;
   size_t scratch0, scratch_stride;
   int nscratch;            // binning streams / scratch blocks of this call
   size_t sort_blocks;      // blocks of one radix pass over N items
@@ -98,6 +98,7 @@ Views views_of(const Plan& p, void* state);
 // ---- launch accounting (every kernel launch of the library is counted; see puv_profile_read) ----
 void count_launches(int n);
 size_t depth_sort_scratch_bytes(size_t N);
+size_t bin_scratch_bytes(size_t N, int ntiles);
 
 // ---- launchers (all asynchronous on `s`) ----
 void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kScanThreads) k_koff_reduce(const uint32_t* __
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
       const uint32_t r = base + threadIdx.x * kScanItems + i;
-      if (r < n) s += rect_tiles(rect[sorted[r]]);
+      if (r < n) s += rect_tiles(rect[sorted ? sorted[r] : r]);
     }
   }
   uint32_t tot;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kScanThreads) k_koff_write(const uint32_t* __r
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     const uint32_t r = base + threadIdx.x * kScanItems + i;
-    t[i] = r < n ? rect_tiles(rect[sorted[r]]) : 0u;
+    t[i] = r < n ? rect_tiles(rect[sorted ? sorted[r] : r]) : 0u;
     s += t[i];
   }
   uint32_t tot;
@@ -137,29 +137,7 @@ __global__ void __launch_bounds__(kScanThreads) k_koff_write(const uint32_t* __r
 }
 
 // Views are binned concurrently on several streams: the arena is carved with atomics (a view's
-// list_base depends on the completion order; its contents do not).
-__global__ void k_view_finalize(ViewHdr* hdr, CallHdr* call, const uint64_t* ktotal) {
-  const uint64_t K = *ktotal;
-  hdr->K = K;
-  atomicAdd((unsigned long long*)&call->arena_need, (unsigned long long)K);
-  const uint64_t base = K < 0xffffffffull ? atomicAdd((unsigned long long*)&call->arena_used, (unsigned long long)K)
-                                          : ~0ull;
-  const bool fits = base != ~0ull && base + K <= call->arena_cap;
-  if (fits) {
-    hdr->list_base = base;
-    hdr->overflow = 0;
-    uint64_t kb = (K + kNbMax - 1) / kNbMax;
-    if (kb < 65536) kb = 65536;
-    hdr->kb = (uint32_t)kb;
-    hdr->nb = (uint32_t)((K + kb - 1) / kb);
-  } else {
-    hdr->list_base = 0;
-    hdr->overflow = 1;
-    call->overflow_any = 1;
-    hdr->kb = 65536;
-    hdr->nb = 0;
-  }
-}
+// list_base depends on the completion order; its contents do not) -- see k_view_finalize2.
 
 // bstart[b] = largest rank r < n_vis with koff[r] <= b*kb  (koff strictly increasing: every rank has >= 1 key)
 __global__ void k_block_starts(const ViewHdr* hdr, const uint32_t* __restrict__ koff, uint32_t* __restrict__ bstart) {
@@ -211,7 +189,7 @@ __device__ uint32_t load_super(SuperGroup& sg, uint32_t r, uint32_t n_vis, uint6
       const uint64_t ks = koff[rr], ke = koff[rr + 1];
       const uint64_t s = ks > klo ? ks : klo, e = ke < khi ? ke : khi;
       if (e > s) {
-        const uint32_t gid = sorted[rr];
+        const uint32_t gid = sorted ? sorted[rr] : rr;
         const uint2 rc = rect[gid];
         const uint32_t x0 = rc.x & 0xffffu, w = (rc.x >> 16) - x0;
         const uint32_t y0 = rc.y & 0xffffu, y1 = rc.y >> 16;
@@ -473,37 +451,284 @@ __global__ void __launch_bounds__(kBinThreads) k_tile_scatter(const ViewHdr* hdr
   }
 }
 
+// ---- two-level tile pass ---------------------------------------------------------------------
+//
+// Level 1 bins the RANKS into super-tiles of kSup x kSup tiles with the stable counting sort
+// above (k_tile_count / k_col_scan / k_tile_ranges / k_tile_scatter over super-tile rects: ~K/10
+// keys at C3).  Level 2 splits every super-tile's rank list into segments of `seglen` ranks; one
+// warp per segment walks 32 ranks at a time and, for each of the kSup^2 tiles of its super-tile,
+// takes a ballot of the lanes whose rect covers the tile: popc(ballot) counts (pass 1), and
+// popc(ballot & lanes-below) is a lane's stable slot inside the tile's run (pass 2), so every
+// tile list comes out in rank = (depth_bits, gid) order with one coalesced run of writes per
+// (32 ranks, tile).
+
+constexpr int kSup = 4;                    // tiles per super-tile side
+constexpr int kSupT = kSup * kSup;         // tiles per super-tile
+constexpr int kSegMin = 512;               // ranks per level-2 segment (at least)
+constexpr int kSegTarget = 32768;          // seglen >= K1 / kSegTarget, so segments <= kSegTarget + nst
+
+__host__ __device__ inline size_t max_segments(int ntiles) { return (size_t)kSegTarget + (size_t)ntiles; }
+
+struct L2Info { uint32_t seglen, nseg, pad0, pad1; };
+
+// Per rank: the tile rect + gid (for level 2) and the super-tile rect (level 1); K = sum of tiles.
+__global__ void __launch_bounds__(256) k_bin_prep(const ViewHdr* hdr, const uint32_t* __restrict__ sorted,
+                                                  const uint2* __restrict__ rect, uint4* __restrict__ rk,
+                                                  uint2* __restrict__ srect, unsigned long long* __restrict__ ktotal) {
+  __shared__ unsigned long long part[8];
+  const uint32_t n = hdr->n_vis;
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t t = 0;
+  if (r < n) {
+    const uint32_t gid = sorted[r];
+    const uint2 rc = rect[gid];
+    rk[r] = make_uint4(rc.x, rc.y, gid, 0u);
+    const uint32_t x0 = rc.x & 0xffffu, x1 = rc.x >> 16, y0 = rc.y & 0xffffu, y1 = rc.y >> 16;
+    t = (x1 - x0) * (y1 - y0);
+    const uint32_t sx0 = x0 / kSup, sx1 = (x1 + kSup - 1) / kSup, sy0 = y0 / kSup, sy1 = (y1 + kSup - 1) / kSup;
+    srect[r] = make_uint2(sx0 | (sx1 << 16), sy0 | (sy1 << 16));
+  }
+  unsigned long long w = __reduce_add_sync(0xffffffffu, t);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = 0;
+    for (int k = 0; k < 8; ++k) b += part[k];
+    if (b) atomicAdd(ktotal, b);
+  }
+}
+
+// Carve this view's final lists (K keys) and its level-1 rank lists (K1) from the arena.
+__global__ void k_view_finalize2(ViewHdr* hdr, CallHdr* call, const unsigned long long* ktotal,
+                                 const uint64_t* k1total, ViewHdr* l1) {
+  const uint64_t K = *ktotal, K1 = *k1total, need = K + K1;
+  hdr->K = K;
+  atomicAdd((unsigned long long*)&call->arena_need, (unsigned long long)need);
+  const uint64_t base = K < 0xffffffffull ? atomicAdd((unsigned long long*)&call->arena_used, (unsigned long long)need)
+                                          : ~0ull;
+  const bool fits = base != ~0ull && base + need <= call->arena_cap;
+  l1->n_vis = hdr->n_vis;
+  l1->K = K1;
+  if (fits) {
+    hdr->list_base = base;
+    hdr->overflow = 0;
+    l1->list_base = base + K;
+    l1->overflow = 0;
+    uint64_t kb = (K1 + kNbMax - 1) / kNbMax;
+    if (kb < 2048) kb = 2048;
+    l1->kb = (uint32_t)kb;
+    l1->nb = (uint32_t)((K1 + kb - 1) / kb);
+  } else {
+    hdr->list_base = 0;
+    hdr->overflow = 1;
+    call->overflow_any = 1;
+    l1->list_base = 0;
+    l1->overflow = 1;
+    l1->kb = 2048;
+    l1->nb = 0;
+  }
+}
+
+// Level-2 segment plan (one block): seglen, segments per super-tile (prefix in segbase), seg -> st.
+__global__ void __launch_bounds__(1024) k_seg_plan(const ViewHdr* l1, const uint32_t* __restrict__ sst,
+                                                   const uint32_t* __restrict__ sen, int nst,
+                                                   uint32_t* __restrict__ segbase, uint32_t* __restrict__ segst,
+                                                   L2Info* info) {
+  __shared__ uint32_t part[1024];
+  __shared__ uint32_t s_len;
+  if (threadIdx.x == 0) {
+    const uint64_t K1 = l1->overflow ? 0 : l1->K;
+    uint64_t len = (K1 + kSegTarget - 1) / kSegTarget;
+    if (len < kSegMin) len = kSegMin;
+    s_len = (uint32_t)len;
+  }
+  __syncthreads();
+  const uint32_t seglen = s_len;
+  const bool ov = l1->overflow != 0;
+  const int per = (nst + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(nst, lo + per);
+  uint32_t s = 0;
+  for (int i = lo; i < hi; ++i) s += ov ? 0u : (sen[i] - sst[i] + seglen - 1) / seglen;
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const uint32_t x = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += x;
+    __syncthreads();
+  }
+  uint32_t run = part[threadIdx.x] - s;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t c = ov ? 0u : (sen[i] - sst[i] + seglen - 1) / seglen;
+    segbase[i] = run;
+    for (uint32_t k = 0; k < c; ++k) segst[run + k] = (uint32_t)i;
+    run += c;
+  }
+  if (threadIdx.x == 1023) {
+    segbase[nst] = part[1023];
+    info->seglen = seglen;
+    info->nseg = part[1023];
+  }
+}
+
+// 16-bit mask of the tiles of super-tile (sx, sy) covered by tile rect q (bit = ly * kSup + lx).
+__device__ __forceinline__ uint32_t cover_mask(const uint4& q, uint32_t sx, uint32_t sy) {
+  const uint32_t x0 = q.x & 0xffffu, x1 = q.x >> 16, y0 = q.y & 0xffffu, y1 = q.y >> 16;
+  const uint32_t bx = sx * kSup, by = sy * kSup;
+  const uint32_t lx0 = x0 > bx ? x0 - bx : 0u, lx1 = min(x1 - bx, (uint32_t)kSup);
+  const uint32_t ly0 = y0 > by ? y0 - by : 0u, ly1 = min(y1 - by, (uint32_t)kSup);
+  const uint32_t row = ((1u << lx1) - 1u) & ~((1u << lx0) - 1u);
+  const uint32_t rows = ((1u << ly1) - 1u) & ~((1u << ly0) - 1u);   // bit per local row
+  uint32_t m = 0;
+#pragma unroll
+  for (int ly = 0; ly < kSup; ++ly) m |= ((rows >> ly) & 1u) ? row << (kSup * ly) : 0u;
+  return m;
+}
+
+// Walk segment `seg` 32 ranks at a time; PASS 1 counts per tile, PASS 2 places.
+template <int PASS>
+__global__ void __launch_bounds__(256) k_seg_walk(const ViewHdr* hdr, const ViewHdr* l1, const L2Info* info,
+                                                  const uint32_t* __restrict__ segbase,
+                                                  const uint32_t* __restrict__ segst,
+                                                  const uint32_t* __restrict__ sst, const uint32_t* __restrict__ sen,
+                                                  const uint32_t* __restrict__ arena, const uint4* __restrict__ rk,
+                                                  int sgx, int gx, int gy, uint32_t* __restrict__ cnt2,
+                                                  const uint32_t* __restrict__ tstart, uint32_t* __restrict__ out) {
+  if (l1->overflow) return;
+  const uint32_t nseg = info->nseg, seglen = info->seglen;
+  const int lane = threadIdx.x & 31;
+  const uint32_t* list1 = arena + l1->list_base;
+  uint32_t* list = out + hdr->list_base;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < nseg; seg += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t st = segst[seg];
+    const uint32_t sx = st % sgx, sy = st / sgx;
+    const uint32_t i0 = sst[st] + (seg - segbase[st]) * seglen;
+    const uint32_t i1 = min(sen[st], i0 + seglen);
+    uint32_t base[kSupT];
+#pragma unroll
+    for (int b = 0; b < kSupT; ++b) {
+      base[b] = 0;
+      if (PASS == 2) {
+        const uint32_t tx = sx * kSup + (b % kSup), ty = sy * kSup + (b / kSup);
+        if (tx < (uint32_t)gx && ty < (uint32_t)gy) base[b] = tstart[ty * gx + tx] + cnt2[(size_t)seg * kSupT + b];
+      }
+    }
+    // software pipeline: the next batch's rank and rect are loaded before this batch is placed
+    uint32_t i = i0 + lane;
+    uint4 q = make_uint4(0, 0, 0, 0);
+    if (i < i1) q = rk[list1[i]];
+    for (uint32_t b0 = i0; b0 < i1; b0 += 32) {
+      const bool valid = b0 + lane < i1;
+      const uint4 cur = q;
+      const uint32_t inx = b0 + 32 + lane;
+      if (inx < i1) q = rk[list1[inx]];
+      const uint32_t m = valid ? cover_mask(cur, sx, sy) : 0u;
+#pragma unroll
+      for (int b = 0; b < kSupT; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (m >> b) & 1u);
+        if (PASS == 2 && ((m >> b) & 1u)) list[base[b] + __popc(bal & lt)] = cur.z;
+        base[b] += __popc(bal);
+      }
+    }
+    if (PASS == 1 && lane < kSupT) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int b = 0; b < kSupT; ++b) c = lane == b ? base[b] : c;
+      cnt2[(size_t)seg * kSupT + lane] = c;
+    }
+  }
+}
+
+// Per tile: exclusive offsets of its super-tile's segments (in place in cnt2) and the tile total.
+// One warp per super-tile, lane b < kSupT walks column b of the super-tile's segment rows (16
+// consecutive words per row: coalesced, and the loads run ahead of the running sum).
+__global__ void __launch_bounds__(256) k_seg_offsets(const ViewHdr* l1, const uint32_t* __restrict__ segbase,
+                                                     int sgx, int nst, int gx, int gy, uint32_t* __restrict__ cnt2,
+                                                     uint32_t* __restrict__ total) {
+  const int st = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, b = threadIdx.x & 31;
+  if (st >= nst || b >= kSupT) return;
+  const int tx = (st % sgx) * kSup + b % kSup, ty = (st / sgx) * kSup + b / kSup;
+  uint32_t run = 0;
+  if (!l1->overflow) {
+    const uint32_t s0 = segbase[st], s1 = segbase[st + 1];
+    uint32_t* c = cnt2 + (size_t)s0 * kSupT + b;
+#pragma unroll 8
+    for (uint32_t k = 0; k < s1 - s0; ++k) {
+      const uint32_t x = c[(size_t)k * kSupT];
+      c[(size_t)k * kSupT] = run;
+      run += x;
+    }
+  }
+  if (tx < gx && ty < gy) total[ty * gx + tx] = run;
+}
+
+size_t bin_scratch_bytes(size_t N, int ntiles) {
+  const size_t ms = max_segments(ntiles);
+  return align_up(16 * N) + align_up(8 * N) + align_up(sizeof(ViewHdr)) + align_up(16) + align_up(sizeof(L2Info)) +
+         3 * align_up(4 * ((size_t)ntiles + 1)) + align_up(4 * ms) + align_up(4 * ms * kSupT);
+}
+
 void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s) {
   char* st = (char*)state;
   const uint32_t* sorted = v.sorted + (size_t)view * p.N;
   const uint2* rect = v.rect + (size_t)view * p.N;
   ViewHdr* hdr = v.hdr + view;
   uint32_t* bsum = (uint32_t*)(st + p.bsum);
-  uint32_t* koff = (uint32_t*)(st + p.koff);
+  uint32_t* koff1 = (uint32_t*)(st + p.koff);
   uint32_t* cnt = (uint32_t*)(st + p.cnt);
   uint32_t* bstart = (uint32_t*)(st + p.bstart);
-  uint64_t* ktot = &hdr->ktotal;  // scratch: K of this view before finalize
   uint32_t* tstart = v.tstart + (size_t)view * p.ntiles;
   uint32_t* tend = v.tend + (size_t)view * p.ntiles;
-  const int nsb = p.N / kScanTile + 1;   // one extra block so koff[n_vis] (= K) is always written
-  k_koff_reduce<<<nsb, kScanThreads, 0, s>>>(sorted, rect, hdr, bsum);
-  k_scan_bsum<<<1, 1024, 0, s>>>(bsum, nsb, ktot);
-  k_koff_write<<<nsb, kScanThreads, 0, s>>>(sorted, rect, hdr, bsum, koff);
-  k_view_finalize<<<1, 1, 0, s>>>(hdr, v.call, ktot);
-  k_block_starts<<<(kNbMax + 255) / 256, 256, 0, s>>>(hdr, koff, bstart);
+  // level-2 scratch (carved from the block at p.bin2)
+  char* b2 = st + p.bin2;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { char* q = b2 + o; o += align_up(bytes); return q; };
+  const int sgx = (p.gx + kSup - 1) / kSup, sgy = (p.gy + kSup - 1) / kSup, nst = sgx * sgy;
+  uint4* rk = (uint4*)take(16 * (size_t)p.N);
+  uint2* srect = (uint2*)take(8 * (size_t)p.N);
+  ViewHdr* l1 = (ViewHdr*)take(sizeof(ViewHdr));
+  unsigned long long* ktot = (unsigned long long*)take(16);
+  L2Info* info = (L2Info*)take(sizeof(L2Info));
+  uint32_t* sst = (uint32_t*)take(4 * ((size_t)p.ntiles + 1));
+  uint32_t* sen = (uint32_t*)take(4 * ((size_t)p.ntiles + 1));
+  uint32_t* segbase = (uint32_t*)take(4 * ((size_t)p.ntiles + 1));
+  uint32_t* segst = (uint32_t*)take(4 * max_segments(p.ntiles));
+  uint32_t* cnt2 = (uint32_t*)take(4 * max_segments(p.ntiles) * kSupT);
+  uint64_t* k1tot = &l1->ktotal;
+
+  cudaMemsetAsync(ktot, 0, 16, s);
+  k_bin_prep<<<(p.N + 255) / 256, 256, 0, s>>>(hdr, sorted, rect, rk, srect, ktot);
+  // level-1 key offsets per rank (super-tile keys), K1
+  const int nsb = p.N / kScanTile + 1;   // one extra block so koff1[n_vis] (= K1) is always written
+  k_koff_reduce<<<nsb, kScanThreads, 0, s>>>(nullptr, srect, hdr, bsum);
+  k_scan_bsum<<<1, 1024, 0, s>>>(bsum, nsb, k1tot);
+  k_koff_write<<<nsb, kScanThreads, 0, s>>>(nullptr, srect, hdr, bsum, koff1);
+  k_view_finalize2<<<1, 1, 0, s>>>(hdr, v.call, ktot, k1tot, l1);
+  k_block_starts<<<(kNbMax + 255) / 256, 256, 0, s>>>(l1, koff1, bstart);
 
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int band_rows = p.gx >= kBandTiles ? 1 : (kBandTiles / p.gx < p.gy ? kBandTiles / p.gx : p.gy);
-  const int nbands = (p.gy + band_rows - 1) / band_rows;
-  k_tile_count<<<4 * nsm, kBinThreads, 0, s>>>(hdr, koff, sorted, rect, bstart, p.gx, p.gy, band_rows, nbands,
-                                              p.ntiles, cnt);
-  k_col_scan<<<(p.ntiles + 31) / 32, 1024, 0, s>>>(hdr, cnt, p.ntiles, tend /* totals */);
+  // level 1: stable counting sort of super-tile keys (ranks) by super-tile
+  const int band_rows = sgx >= kBandTiles ? 1 : (kBandTiles / sgx < sgy ? kBandTiles / sgx : sgy);
+  const int nbands = (sgy + band_rows - 1) / band_rows;
+  k_tile_count<<<4 * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
+                                              cnt);
+  k_col_scan<<<(nst + 31) / 32, 1024, 0, s>>>(l1, cnt, nst, sen /* totals */);
+  k_tile_ranges<<<1, 1024, 0, s>>>(sen, nst, sst, sen);
+  k_tile_scatter<<<4 * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
+                                                cnt, sst, arena + 0);
+  // level 2: per-tile lists from the super-tile rank lists
+  k_seg_plan<<<1, 1024, 0, s>>>(l1, sst, sen, nst, segbase, segst, info);
+  const int wblocks = 8 * nsm;   // 8 warps per block, grid-stride over segments
+  k_seg_walk<1><<<wblocks, 256, 0, s>>>(hdr, l1, info, segbase, segst, sst, sen, arena, rk, sgx, p.gx, p.gy, cnt2,
+                                        nullptr, nullptr);
+  k_seg_offsets<<<(nst + 7) / 8, 256, 0, s>>>(l1, segbase, sgx, nst, p.gx, p.gy, cnt2, tend /* totals */);
   k_tile_ranges<<<1, 1024, 0, s>>>(tend, p.ntiles, tstart, tend);
-  k_tile_scatter<<<4 * nsm, kBinThreads, 0, s>>>(hdr, koff, sorted, rect, bstart, p.gx, p.gy, band_rows, nbands,
-                                                p.ntiles, cnt, tstart, arena);
-  count_launches(9);
+  k_seg_walk<2><<<wblocks, 256, 0, s>>>(hdr, l1, info, segbase, segst, sst, sen, arena, rk, sgx, p.gx, p.gy, cnt2,
+                                        tstart, arena);
+  count_launches(16);
 }
 
 }  // namespace puv

@@ -227,8 +227,11 @@ def test_arena_overflow_flag_and_retry():
     ov, need = puv.check_overflow(R.state, 1)
     planes, occ, _ = oracle_scene(sc)
     P = orc.project(planes, occ, sc.cameras[0])
-    K = int(P["tiles"][P["visible"] == 1].sum())
-    assert ov and need == 4 * K
+    vis = P[P["visible"] == 1]
+    K = int(vis["tiles"].sum())
+    # + the level-1 keys of the binning: super-tiles of 4 x 4 tiles (include/puv.h)
+    K1 = int((((vis["x1"] + 3) // 4 - vis["x0"] // 4) * ((vis["y1"] + 3) // 4 - vis["y0"] // 4)).sum())
+    assert ov and need == 4 * (K + K1)
     assert torch.all(img == 0)     # overflowed view renders only the (black) background
     img2 = R.forward(g["atlas"], g["occ"])   # grows the arena and re-renders
     assert R.arena.numel() >= 4 * K

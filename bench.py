@@ -170,10 +170,10 @@ def stage_work(stage, c, D):
         return "hbm", 4 * N + 4 * nv
     if stage == "bin":              # read rank rects, write every key once, ranges
         return "hbm", 8 * nv + 4 * K + 8 * c["ntiles"]
-    if stage == "raster_fwd":       # fp64 lane-ops of the value path: 22 per composited pair
-        return "alu_fp64", 22 * P
-    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 40
-        return "alu_fp64", 40 * P
+    if stage == "raster_fwd":       # fp64 lane-ops of the value path: 18 per composited pair
+        return "alu_fp64", 18 * P
+    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 36
+        return "alu_fp64", 36 * P
     if stage == "project_bwd":      # read 2D grads + params, RMW texel grads
         return "hbm", 72 * nv + (D * 4 * 3 * N) / c["views"]
     if stage == "loss":
@@ -263,11 +263,8 @@ def main():
         t_dev = torch.empty_like(targets)
 
         def e2e_step():
-            a_dev.copy_(atlas_host, non_blocking=True)
-            t_dev.copy_(tg_host, non_blocking=True)
             grad.zero_()
-            l = stepper.step(a_dev, occ, t_dev, grad)
-            loss_host.copy_(l, non_blocking=True)
+            stepper.step_host(atlas_host, occ, tg_host, grad, a_dev, t_dev, loss_host)
 
         e2e_step()
         torch.cuda.synchronize()

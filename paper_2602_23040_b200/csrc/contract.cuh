@@ -76,49 +76,43 @@ PUV_DEV float pair_power(float mx, float my, float ha, float nb, float hc, float
 }
 
 // ---- fp64 value path helpers (not part of the contract) ---------------------------------------
-// exp(x) = 2^m * 2^(j/64) * e^r,  k = rint(64 x / ln2) = 64 m + j,  r = x - k ln2/64 (one fma:
-// the rounding of ln2/64 costs |k| * 1.2e-18, < 1e-13 over the valid range), |r| <= ln2/128,
-// e^r by its degree-4 Taylor polynomial (truncation < 4e-14).  Measured max relative error vs
-// libm over [-700, 0]: 1.2e-13 -- far below what the gradient tolerance needs.
-// `tab` = 2^(j/64), j < 64, staged in shared memory by the caller (exp64_table_fill).
+// exp(x) = 2^m * 2^(j/256) * e^r,  k = rint(256 x / ln2) = 256 m + j,  r = x - k ln2/256 (one fma:
+// the rounding of ln2/256 costs |k| * 3e-19 < 1e-13 over the valid range), |r| <= ln2/512,
+// e^r by its degree-3 Taylor polynomial (truncation < 1.5e-13).  Max relative error vs libm over
+// [-700, 0] below 3e-13 (tools/exp64_check.py) -- far below what the gradient tolerance needs
+// (DESIGN.md §5).  `tab` = 2^(j/256), j < 256, staged in shared memory (exp64_table_fill).
 // Valid for x in [-700, 1]; for far-out x (inactive pixels of the branch-free backward) the
 // result is garbage but finite-or-inf, and the callers select it away.
+constexpr int kExpTab = 256;
 PUV_DEV void exp64_table_fill(double* tab) {
-  for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = exp2((double)j / 64.0);
+  for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = exp2((double)j / kExpTab);
 }
 
 PUV_DEV double exp64(double x, const double* tab) {
-  constexpr double kInvL = 92.33248261689366;            // 64 / ln 2
-  constexpr double kL = 0.010830424696249145;            // ln 2 / 64
+  constexpr double kInvL = 369.3299304675746;            // 256 / ln 2
+  constexpr double kL = 0.0027076061740622863;           // ln 2 / 256
   constexpr double kShift = 6755399441055744.0;          // 1.5 * 2^52: rint by addition
   const double t = fma(x, kInvL, kShift);
-  const int k = (int)__double2loint(t);                  // low word = rint(64 x / ln2) (two's complement)
+  const int k = (int)__double2loint(t);                  // low word = rint(256 x / ln2) (two's complement)
   const double r = fma(-(t - kShift), kL, x);
-  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
-  p = fma(r, p, 0.5);
+  double p = fma(r, 1.0 / 6.0, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);
-  const double v = tab[k & 63] * p;
-  return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+  const double v = tab[k & (kExpTab - 1)] * p;
+  return __hiloint2double(__double2hiint(v) + ((k >> 8) << 20), __double2loint(v));
 }
 
-// Gaussian exponent in fp64 from the pixel offset (dx, dy) = mean - pixel; also returns the
-// second-order monomials (shared by K5 and K6 so both evaluate the same rounded value).
-PUV_DEV double power64(double ha, double nb, double hc, double dx, double dy, double& dxx, double& dxy,
-                       double& dyy) {
-  dxx = dx * dx;
-  dxy = dx * dy;
-  dyy = dy * dy;
-  return fma(ha, dxx, fma(nb, dxy, hc * dyy));
-}
+// Gaussian exponent in fp64, power = ha dx^2 + dy (nb dx + hc dy) with (dx, dy) = mean - pixel,
+// from the column terms hadxx = ha dx^2 and nbdx = nb dx (shared by the pixels of a thread, which
+// sit in one pixel column).  K5 and K6 evaluate it identically.
+PUV_DEV double power64(double hc, double hadxx, double nbdx, double dy) { return fma(dy, fma(hc, dy, nbdx), hadxx); }
 
-// 1/y for y in [0.01, 1]: MUFU fp64 reciprocal estimate + two Newton steps (~1 ulp)
+// 1/y for y in [0.01, 1]: MUFU fp64 reciprocal estimate (~2^-23 relative) + one Newton step
+// (error squared: ~2^-46 = 1.4e-14 relative, far below what the gradients need)
 PUV_DEV double rcp64(double y) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
-  double e = fma(-y, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-y, r, 1.0);
+  const double e = fma(-y, r, 1.0);
   return fma(r, e, r);
 }
 

@@ -1,11 +1,11 @@
 // K5 k_raster_fwd — per-tile front-to-back compositing (row a5).
 //
-// One 128-thread block per 16x16 tile, two pixels per thread ("tile-based
-// rasterizer"; semantics R9).  Warp w owns the 8x8 quadrant (8(w&1), 8(w>>1)); lane l owns
-// column l & 7 and rows (l >> 3) + 4k, k < 2 (the layout of K6).  The tile's sorted Gaussian list
-// is consumed in batches of 128: each thread gathers one entry into shared memory (contract
-// record A, B and the fp64 value record; LDS broadcast on use), so one pair of record loads and
-// one loop step serve both pixels of a thread.  Every lane runs the skip test of both its pixels;
+// One block per 16x16 tile, PPT pixels per thread in one column ("tile-based
+// rasterizer"; semantics R9).  Warp w owns the 8-column block 8(w&1) of rows 4 PPT (w>>1) ..;
+// lane l owns column l & 7 and rows (l >> 3) + 4k, k < PPT (the layout of K6).  The tile's
+// sorted Gaussian list is consumed in batches of 128 entries gathered into shared memory
+// (contract record A, B and the fp64 value record; LDS broadcast on use), so one set of record
+// loads and one loop step serve all pixels of a thread.  Every lane runs the skip test of both its pixels;
 // the composite runs under a per-pixel predicate and only when some pixel of the warp composites.
 // A warp stops walking a batch as soon as all its pixels have terminated (vote), the block stops
 // fetching batches once all 256 pixels have (syncthreads_count).
@@ -18,22 +18,40 @@
 
 namespace puv {
 
-constexpr int kFwdPPT = 2;                               // pixels per thread
-constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128
-constexpr int kFwdBatch = kRasterThreads;                // entries staged per batch
+#ifndef PUV_FWD_PPT
+#define PUV_FWD_PPT 2
+#endif
+constexpr int kFwdPPT = PUV_FWD_PPT;                     // pixels per thread (one column, rows r + 4k)
+constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128 (PPT 2) or 64 (PPT 4)
+constexpr int kFwdBatch = 128;                           // entries staged per batch
+
+template <int P>
+__device__ __forceinline__ bool all_of(const bool (&b)[P]) {
+  bool r = true;
+#pragma unroll
+  for (int k = 0; k < P; ++k) r = r && b[k];
+  return r;
+}
+template <int P>
+__device__ __forceinline__ bool any_of(const bool (&b)[P]) {
+  bool r = false;
+#pragma unroll
+  for (int k = 0; k < P; ++k) r = r || b[k];
+  return r;
+}
 
 __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* __restrict__ arena, Views v, int view,
                                                               int N, int W, int H, int gx, int ntiles, float bg0,
                                                               float bg1, float bg2, float* __restrict__ image) {
   __shared__ float4 sA[kFwdBatch], sB[kFwdBatch];
   __shared__ double2 sD[5][kFwdBatch];
-  __shared__ double sExp[64];
+  __shared__ double sExp[kExpTab];
   exp64_table_fill(sExp);
   const int tile = blockIdx.x;
   const int tx = tile % gx, ty = tile / gx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-  const int py0 = ty * kTile + (warp >> 1) * 8 + (lane >> 3);
+  const int py0 = ty * kTile + (warp >> 1) * 4 * kFwdPPT + (lane >> 3);
   const ViewHdr& hdr = v.hdr[view];
   uint32_t start = 0, end = 0;
   if (!hdr.overflow) {
@@ -59,19 +77,25 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
     last[k] = 0;
     done[k] = !(px < W && py0 + 4 * k < H);
   }
-  uint32_t n_exam = 0, n_comp = 0;
-  for (uint32_t b0 = start; b0 < end; b0 += kFwdBatch) {
-    if (__syncthreads_count(done[0] && done[1]) == kRasterThreads) break;
-    const uint32_t idx = b0 + threadIdx.x;
-    if (idx < end) {
-      const uint32_t g = list[idx];
-      sA[threadIdx.x] = rec[3 * (size_t)g + 0];
-      sB[threadIdx.x] = rec[3 * (size_t)g + 1];
+  // examined pairs of a pixel = entries walked until it terminated (inclusive) or the list ended
+  uint32_t exam[kFwdPPT], n_comp = 0;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) sD[k][threadIdx.x] = rec64[5 * (size_t)g + k];
+  for (int k = 0; k < kFwdPPT; ++k) exam[k] = 0;
+  for (uint32_t b0 = start; b0 < end; b0 += kFwdBatch) {
+    if (__syncthreads_count(all_of(done)) == kRasterThreads) break;
+#pragma unroll
+    for (int i = threadIdx.x; i < kFwdBatch; i += kRasterThreads) {
+      const uint32_t idx = b0 + i;
+      if (idx < end) {
+        const uint32_t g = list[idx];
+        sA[i] = rec[3 * (size_t)g + 0];
+        sB[i] = rec[3 * (size_t)g + 1];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) sD[k][i] = rec64[5 * (size_t)g + k];
+      }
     }
     __syncthreads();
-    const int n = __all_sync(0xffffffffu, done[0] && done[1]) ? 0 : (int)min((uint32_t)kFwdBatch, end - b0);
+    const int n = __all_sync(0xffffffffu, all_of(done)) ? 0 : (int)min((uint32_t)kFwdBatch, end - b0);
     for (int j = 0; j < n; ++j) {
       const float4 A = sA[j];
       const float4 B = sB[j];
@@ -81,9 +105,13 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
       for (int k = 0; k < kFwdPPT; ++k) {
         power[k] = pair_power(A.x, A.y, A.z, A.w, B.x, fi, fj[k]);
         hit[k] = !done[k] && !(power[k] > 0.0f || power[k] < B.y);
-        n_exam += done[k] ? 0u : 1u;
       }
-      if (!__any_sync(0xffffffffu, hit[0] || hit[1])) continue;
+      if (!__any_sync(0xffffffffu, any_of(hit))) continue;
+      // fp64 record and the column terms shared by both pixels (same px): dx, ha dx^2, nb dx
+      const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
+      const double d4x = sD[4][j].x;
+      const double dx = d0.x - di;
+      const double hadxx = d1.x * (dx * dx), nbdx = d1.y * dx;
 #pragma unroll
       for (int k = 0; k < kFwdPPT; ++k) {
         if (!hit[k]) continue;
@@ -93,16 +121,14 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
         const float Tn = mul(T[k], sub(1.0f, alpha));
         if (Tn < 1e-4f) {
           done[k] = true;
+          exam[k] = b0 + j + 1 - start;
           continue;
         }
         T[k] = Tn;
         last[k] = b0 + j + 1 - start;
         ++n_comp;
         // fp64 value of the composited pair
-        const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
-        const double d4x = sD[4][j].x;
-        double dxx, dxy, dyy;
-        const double pw = power64(d1.x, d1.y, d2.x, d0.x - di, d0.y - dj[k], dxx, dxy, dyy);
+        const double pw = power64(d2.x, hadxx, nbdx, d0.y - dj[k]);
         const double a64 = capped ? 0.99 : d2.y * exp64(pw, sExp);
         const double w = a64 * T64[k];
         C[k][0] = fma(d3.x, w, C[k][0]);
@@ -110,9 +136,12 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* _
         C[k][2] = fma(d4x, w, C[k][2]);
         T64[k] -= w;   // T64 * (1 - a64)
       }
-      if (__all_sync(0xffffffffu, done[0] && done[1])) break;
+      if (__all_sync(0xffffffffu, all_of(done))) break;
     }
   }
+  uint32_t n_exam = 0;
+#pragma unroll
+  for (int k = 0; k < kFwdPPT; ++k) n_exam += done[k] ? exam[k] : (px < W && py0 + 4 * k < H ? end - start : 0u);
   {  // pair statistics (one atomic per warp)
     const uint32_t we = __reduce_add_sync(0xffffffffu, n_exam), wc = __reduce_add_sync(0xffffffffu, n_comp);
     if (lane == 0 && (we | wc)) {

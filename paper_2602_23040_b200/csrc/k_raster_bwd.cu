@@ -1,8 +1,10 @@
 // K6 k_raster_bwd — per-tile gradient of the front-to-back composite (row a7).
 //
-// One 128-thread block (4 warps) per (16x16 tile, view) — all views of a call in one launch;
-// warp w owns the 8x8 pixel quadrant (8(w&1), 8(w>>1)); lane l owns column l & 7 and rows
-// (l >> 3) + 4k, k < PPT = 2.  Every decision (skip test R1, alpha cap, composited set R14) is
+// One 64-thread block (2 warps) per (16x16 tile, view) — all views of a call in one launch;
+// warp w owns the 8-column half 8w of the tile; lane l owns column l & 7 and rows (l >> 3) + 4k,
+// k < PPT = 4 (PPT = 2 with 4 warps of 8x8 quadrants is the -DPUV_BWD_PPT=2 build).  Four pixels
+// per thread halve the per-pixel share of the per-entry warp reduction, which bounds the
+// shared-memory pipe at two pixels per thread (ncu: 87% -> 57% of its wavefronts).  Every decision (skip test R1, alpha cap, composited set R14) is
 // replayed with the fp32 contract exactly as K5 took it; every VALUE is fp64.
 // Single pass in front-to-back order, using the pixel's full colour C from K5.  With dC = dL/dC
 // (3 channels) only the scalar projections of the colours are needed:
@@ -24,31 +26,45 @@
 
 namespace puv {
 
-constexpr int kBwdPPT = 2;                                 // pixels per thread
-constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128
+#ifndef PUV_BWD_PPT
+#define PUV_BWD_PPT 4
+#endif
+#ifndef PUV_BWD_MINB
+#define PUV_BWD_MINB 8
+#endif
+constexpr int kBwdPPT = PUV_BWD_PPT;                       // pixels per thread (one column, rows r + 4k)
+constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128 (PPT 2) or 64 (PPT 4)
+constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4-bank skew per row
 constexpr int kBwdBatch = 128;                             // entries staged per batch
 
-constexpr int kRedStride = 9;   // doubles per lane in the per-warp transpose buffer
-
-// Sum the 9 per-lane values x[0..8] over the warp through shared memory: every lane stores its 9
-// values, lanes 3v, 3v+1, 3v+2 (v < 9) each sum value v over a third of the lanes (11/11/10),
-// and two shuffles fold the thirds into lane 3v.  About 40 instructions per entry, against ~90
-// for a select-based transposing shuffle butterfly.  `buf` is the warp's 32 x 9 slice.
+// Sum the 9 per-lane values x[0..8] over the warp through shared memory: lane l stores x[k] at
+// buf[34 k + l] (conflict-free), then lanes 3v, 3v+1, 3v+2 (v < 9) sum value v over lanes
+// [0, 12), [12, 24), [24, 32) with 16-byte loads, and two shuffles fold the thirds into lane 3v.
+// The row stride of 34 doubles skews row v by 4v banks, so the 27 reading lanes spread over the
+// 8 four-bank groups ((v + 6 part) mod 8): 4 wavefronts per 16-byte load, the minimum.  About
+// 35 instructions per entry.  `buf` is the warp's 9 x 34 slice (16-byte aligned).
 __device__ __forceinline__ double warp_sum9(const double (&x)[9], double* buf, int lane) {
 #pragma unroll
-  for (int k = 0; k < 9; ++k) buf[lane * kRedStride + k] = x[k];
+  for (int k = 0; k < 9; ++k) buf[kRedRow * k + lane] = x[k];
   __syncwarp();
   const int v = lane / 3, part = lane - 3 * v;
   double s0 = 0.0, s1 = 0.0;
   if (lane < 27) {
-    const int l0 = 11 * part, n = part == 2 ? 10 : 11;
-    const double* col = buf + l0 * kRedStride + v;
+    const double2* col = reinterpret_cast<const double2*>(buf + kRedRow * v + 12 * part);
 #pragma unroll
-    for (int i = 0; i < 10; i += 2) {
-      s0 += col[i * kRedStride];
-      s1 += col[(i + 1) * kRedStride];
+    for (int i = 0; i < 4; ++i) {
+      const double2 q = col[i];
+      s0 += q.x;
+      s1 += q.y;
     }
-    if (n == 11) s0 += col[10 * kRedStride];
+    if (part < 2) {
+#pragma unroll
+      for (int i = 4; i < 6; ++i) {
+        const double2 q = col[i];
+        s0 += q.x;
+        s1 += q.y;
+      }
+    }
   }
   __syncwarp();
   double s = s0 + s1;
@@ -57,15 +73,15 @@ __device__ __forceinline__ double warp_sum9(const double (&x)[9], double* buf, i
   return s + p1 + p2;   // valid in lanes 3v, v < 9
 }
 
-__global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int N,
+__global__ void __launch_bounds__(kBwdThreads, PUV_BWD_MINB) k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int N,
                                                            int W, int H, int gx, int ntiles,
                                                            const float* __restrict__ dL_dimages) {
   __shared__ float4 sA[kBwdBatch], sB[kBwdBatch];
   __shared__ double2 sD[5][kBwdBatch];
   __shared__ uint32_t sG[kBwdBatch];
   __shared__ uint32_t smax[kBwdThreads / 32];
-  __shared__ double sRed[kBwdThreads / 32][32 * kRedStride];
-  __shared__ double sExp[64];
+  __shared__ __align__(16) double sRed[kBwdThreads / 32][kRedRow * 9];
+  __shared__ double sExp[kExpTab];
   exp64_table_fill(sExp);
   const int tile = blockIdx.x, view = blockIdx.y;
   const int tx = tile % gx, ty = tile / gx;
@@ -80,7 +96,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
   const size_t HW = (size_t)W * H;
   const float* dL_dimage = dL_dimages + (size_t)view * 3 * HW;
   float fi[kBwdPPT], fj[kBwdPPT];
-  double di[kBwdPPT], dj[kBwdPPT];
+  double di = 0.0, dj[kBwdPPT];
   uint32_t last[kBwdPPT];
   double dC[kBwdPPT][3], Sd[kBwdPPT], T[kBwdPPT];
   uint32_t tlast = 0;
@@ -88,10 +104,10 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
   for (int k = 0; k < kBwdPPT; ++k) {
     // compact 8x8 warp footprint: warp w owns quadrant (8(w&1), 8(w>>1)), lane l column l&7, rows (l>>3)+4k
     const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-    const int py = ty * kTile + (warp >> 1) * 8 + (lane >> 3) + 4 * k;
+    const int py = ty * kTile + (warp >> 1) * 4 * kBwdPPT + (lane >> 3) + 4 * k;
     fi[k] = (float)px;
     fj[k] = (float)py;
-    di[k] = px;
+    di = px;   // the same column for every k
     dj[k] = py;
     last[k] = 0;
     T[k] = 1.0;
@@ -152,14 +168,18 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
       const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
       const double cb = sD[4][j].x;
       const double o = d2.y;
+      // the thread's pixels share the column px: dx and its terms are computed once, and the
+      // dx-only moments follow from the thread's sum of GdL (Mx = dx S, Mxx = dx^2 S)
+      const double dx = d0.x - di, dxx = dx * dx;
+      const double hadxx = d1.x * dxx, nbdx = d1.y * dx;
       double gv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // Mx, My, Mxx, Mxy, Myy, sum GdL, colour r, g, b
+      double sdy = 0.0;                              // sum GdL dy (-> Mxy = dx sdy)
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const double dx = d0.x - di[k], dy = d0.y - dj[k];
-        double dxx, dxy, dyy;
-        const double pw = power64(d1.x, d1.y, d2.x, dx, dy, dxx, dxy, dyy);
-        const double G = exp64(pw, sExp);
-        const double a = act[k] ? (cap[k] ? 0.99 : o * G) : 0.0;
+        const double dy = d0.y - dj[k];
+        const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
+        double a = act[k] ? o * G : 0.0;
+        if (__builtin_expect(may_cap, 0)) a = cap[k] ? 0.99 : a;     // warp-uniform, rare
         const double aT = a * T[k];
         const double cd = fma(dC[k][0], d3.x, fma(dC[k][1], d3.y, dC[k][2] * cb));
         Sd[k] = fma(-cd, aT, Sd[k]);
@@ -167,15 +187,17 @@ __global__ void __launch_bounds__(kBwdThreads) k_raster_bwd(const uint32_t* __re
         gv[6] = fma(aT, dC[k][0], gv[6]);
         gv[7] = fma(aT, dC[k][1], gv[7]);
         gv[8] = fma(aT, dC[k][2], gv[8]);
-        const double GdL = (act[k] && !cap[k]) ? G * dLda : 0.0;
+        double GdL = act[k] ? G * dLda : 0.0;
+        if (__builtin_expect(may_cap, 0)) GdL = cap[k] ? 0.0 : GdL;  // capped: no gradient through alpha
         gv[5] += GdL;
-        gv[0] = fma(GdL, dx, gv[0]);
-        gv[1] = fma(GdL, dy, gv[1]);
-        gv[2] = fma(GdL, dxx, gv[2]);
-        gv[3] = fma(GdL, dxy, gv[3]);
-        gv[4] = fma(GdL, dyy, gv[4]);
+        sdy = fma(GdL, dy, sdy);
+        gv[4] = fma(GdL * dy, dy, gv[4]);
         T[k] -= aT;                                          // T_{k+1} = T_k (1 - a_k)
       }
+      gv[0] = dx * gv[5];
+      gv[1] = sdy;
+      gv[2] = dxx * gv[5];
+      gv[3] = dx * sdy;
       // raw moments into the (view, Gaussian) slot; K7 turns them into dL/d(mx, my, ha, nb, hc)
       const double s = warp_sum9(gv, sRed[warp], lane);
       if (lane < 27 && lane % 3 == 0) atomicAdd(g2 + 9 * (size_t)sG[j] + lane / 3, s);

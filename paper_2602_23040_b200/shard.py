@@ -56,5 +56,29 @@ class ShardedStep:
         reduce_gradients(grad, self.loss, self.world, self.group)
         return self.loss
 
+    def step_host(self, atlas_host, occ, targets_host, grad, atlas_dev, targets_dev, loss_host, mask=None):
+        """The same step from HOST inputs (the end-to-end call): the atlas is copied in first on the
+        current stream (K1 reads all of it), the targets on a side copy stream so that their
+        host->device transfer overlaps the forward render; the loss kernel waits for them.  The
+        (rank-summed) loss is read back into `loss_host`.  Host tensors must be pinned for the
+        copies to be asynchronous."""
+        cur = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+            self._targets_ready = torch.cuda.Event()
+        self._copy_stream.wait_stream(cur)          # targets_dev is free once the previous step's loss ran
+        with torch.cuda.stream(self._copy_stream):
+            targets_dev.copy_(targets_host, non_blocking=True)
+            self._targets_ready.record(self._copy_stream)
+        atlas_dev.copy_(atlas_host, non_blocking=True)
+        puv.render_views(self.R.layout, atlas_dev, occ, self.cams, self.R.opts, self.images, self.R.state,
+                         self.R.arena)
+        cur.wait_event(self._targets_ready)
+        puv.l2_loss_grad(self.images, targets_dev, self.dL, self.loss)
+        self.R.backward(atlas_dev, occ, self.dL, grad=grad, mask=mask)
+        reduce_gradients(grad, self.loss, self.world, self.group)
+        loss_host.copy_(self.loss, non_blocking=True)
+        return loss_host
+
     def overflowed(self) -> bool:
         return puv.check_overflow(self.R.state, len(self.views))[0]

@@ -8,6 +8,8 @@
 #pragma once
 #include <cstdint>
 
+#include "exp2_table.h"
+
 namespace puv {
 
 #define PUV_DEV __device__ __forceinline__
@@ -85,7 +87,7 @@ PUV_DEV float pair_power(float mx, float my, float ha, float nb, float hc, float
 // result is garbage but finite-or-inf, and the callers select it away.
 constexpr int kExpTab = 256;
 PUV_DEV void exp64_table_fill(double* tab) {
-  for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = exp2((double)j / kExpTab);
+  for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = kExp2Tab256[j];   // exp2_table.h
 }
 
 PUV_DEV double exp64(double x, const double* tab) {

@@ -17,7 +17,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpuv.so")
+# PUV_LIB: an alternative build of the same library (A/B timing of kernel variants, tools/ab_raster.py)
+LIB_PATH = os.environ.get("PUV_LIB") or os.path.join(_HERE, "libpuv.so")
 MAX_LEVELS = 16
 
 _status = {0: "PUV_OK", -1: "PUV_E_INVALID_ARGUMENT", -2: "PUV_E_INVALID_CONFIG", -3: "PUV_E_LAYOUT_OVERFLOW",

@@ -23,7 +23,18 @@ namespace puv {
 #endif
 constexpr int kFwdPPT = PUV_FWD_PPT;                     // pixels per thread (one column, rows r + 4k)
 constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128 (PPT 2) or 64 (PPT 4)
-constexpr int kFwdBatch = 128;                           // entries staged per batch
+#ifndef PUV_FWD_MINB
+#define PUV_FWD_MINB 0
+#endif
+#if PUV_FWD_MINB > 0
+#define PUV_FWD_BOUNDS __launch_bounds__(kTile * kTile / PUV_FWD_PPT, PUV_FWD_MINB)
+#else
+#define PUV_FWD_BOUNDS __launch_bounds__(kTile * kTile / PUV_FWD_PPT)
+#endif
+#ifndef PUV_FWD_BATCH
+#define PUV_FWD_BATCH 128
+#endif
+constexpr int kFwdBatch = PUV_FWD_BATCH;                 // entries staged per batch
 
 template <int P>
 __device__ __forceinline__ bool all_of(const bool (&b)[P]) {
@@ -40,7 +51,7 @@ __device__ __forceinline__ bool any_of(const bool (&b)[P]) {
   return r;
 }
 
-__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(const uint32_t* __restrict__ arena, Views v, int view,
+__global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, Views v, int view,
                                                               int N, int W, int H, int gx, int ntiles, float bg0,
                                                               float bg1, float bg2, float* __restrict__ image) {
   __shared__ float4 sA[kFwdBatch], sB[kFwdBatch];

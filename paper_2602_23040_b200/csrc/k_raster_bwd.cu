@@ -19,7 +19,7 @@
 // K7 applies the (linear) o-scaling and the conic mixing once per (view, Gaussian).
 // The per-pixel body is branch-free (inactive pixels get a = 0 and masked terms), so the
 // pixels' fp64 chains interleave.  A thread sums the 9 moments of an entry over its pixels; the
-// warp sums them through a shared-memory transpose (warp_sum9) and 9 lanes issue one fp64 atomic
+// warp sums them with a transposing shuffle butterfly and 9 lanes issue one fp64 atomic
 // each into the (view, Gaussian) slot.
 #include "contract.cuh"
 #include "internal.cuh"
@@ -30,14 +30,23 @@ namespace puv {
 #define PUV_BWD_PPT 4
 #endif
 #ifndef PUV_BWD_MINB
-#define PUV_BWD_MINB 8
+#define PUV_BWD_MINB 0
+#endif
+#if PUV_BWD_MINB > 0
+#define PUV_BWD_BOUNDS __launch_bounds__(kTile * kTile / PUV_BWD_PPT, PUV_BWD_MINB)
+#else
+#define PUV_BWD_BOUNDS __launch_bounds__(kTile * kTile / PUV_BWD_PPT)
 #endif
 constexpr int kBwdPPT = PUV_BWD_PPT;                       // pixels per thread (one column, rows r + 4k)
 constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128 (PPT 2) or 64 (PPT 4)
 constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4-bank skew per row
-constexpr int kBwdBatch = 128;                             // entries staged per batch
+#ifndef PUV_BWD_BATCH
+#define PUV_BWD_BATCH 64
+#endif
+constexpr int kBwdBatch = PUV_BWD_BATCH;                   // entries staged per batch
 
-// Sum the 9 per-lane values x[0..8] over the warp through shared memory: lane l stores x[k] at
+// Alternative reduction (-DPUV_BWD_SMEM_RED).  Sum the 9 per-lane values x[0..8] over the warp
+// through shared memory: lane l stores x[k] at
 // buf[34 k + l] (conflict-free), then lanes 3v, 3v+1, 3v+2 (v < 9) sum value v over lanes
 // [0, 12), [12, 24), [24, 32) with 16-byte loads, and two shuffles fold the thirds into lane 3v.
 // The row stride of 34 doubles skews row v by 4v banks, so the 27 reading lanes spread over the
@@ -73,14 +82,41 @@ __device__ __forceinline__ double warp_sum9(const double (&x)[9], double* buf, i
   return s + p1 + p2;   // valid in lanes 3v, v < 9
 }
 
-__global__ void __launch_bounds__(kBwdThreads, PUV_BWD_MINB) k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int N,
+// Default reduction: transposing shuffle butterfly (8 values in 9 double shuffles, v8 in 5);
+// lane l ends with the total of value (l >> 2) & 7, v8 in all lanes.  A/B on one B200 (C3, 64
+// views, tools/ab_raster.py): 54.4 ms against 55.6 ms for the shared-memory transpose below
+// (-DPUV_BWD_SMEM_RED), which moves more bytes through the MIO pipe per entry.
+__device__ __forceinline__ double warp_reduce9_shfl(double (&x)[9]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int level = 0; level < 3; ++level) {
+    const int half = 4 >> level;
+    const int off = 16 >> level;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = upper ? x[i] : x[i + half];
+      const double keep = upper ? x[i + half] : x[i];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  double s = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x[8] += __shfl_xor_sync(0xffffffffu, x[8], off);
+  return s;
+}
+
+__global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int N,
                                                            int W, int H, int gx, int ntiles,
                                                            const float* __restrict__ dL_dimages) {
   __shared__ float4 sA[kBwdBatch], sB[kBwdBatch];
   __shared__ double2 sD[5][kBwdBatch];
   __shared__ uint32_t sG[kBwdBatch];
   __shared__ uint32_t smax[kBwdThreads / 32];
+#ifdef PUV_BWD_SMEM_RED
   __shared__ __align__(16) double sRed[kBwdThreads / 32][kRedRow * 9];
+#endif
   __shared__ double sExp[kExpTab];
   exp64_table_fill(sExp);
   const int tile = blockIdx.x, view = blockIdx.y;
@@ -95,20 +131,18 @@ __global__ void __launch_bounds__(kBwdThreads, PUV_BWD_MINB) k_raster_bwd(const 
   double* g2 = v.grad2d + (size_t)view * N * 9;
   const size_t HW = (size_t)W * H;
   const float* dL_dimage = dL_dimages + (size_t)view * 3 * HW;
-  float fi[kBwdPPT], fj[kBwdPPT];
-  double di = 0.0, dj[kBwdPPT];
+  // pixel k of a thread sits at (px, py0 + 4k): one column, so x-terms are shared and the
+  // row coordinates are formed on the fly (exact: small integers)
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int py0 = ty * kTile + (warp >> 1) * 4 * kBwdPPT + (lane >> 3);
+  const float fi = (float)px, fj0 = (float)py0;
+  const double di = px, dj0 = py0;
   uint32_t last[kBwdPPT];
   double dC[kBwdPPT][3], Sd[kBwdPPT], T[kBwdPPT];
   uint32_t tlast = 0;
 #pragma unroll
   for (int k = 0; k < kBwdPPT; ++k) {
-    // compact 8x8 warp footprint: warp w owns quadrant (8(w&1), 8(w>>1)), lane l column l&7, rows (l>>3)+4k
-    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-    const int py = ty * kTile + (warp >> 1) * 4 * kBwdPPT + (lane >> 3) + 4 * k;
-    fi[k] = (float)px;
-    fj[k] = (float)py;
-    di = px;   // the same column for every k
-    dj[k] = py;
+    const int py = py0 + 4 * k;
     last[k] = 0;
     T[k] = 1.0;
     Sd[k] = 0.0;
@@ -158,7 +192,7 @@ __global__ void __launch_bounds__(kBwdThreads, PUV_BWD_MINB) k_raster_bwd(const 
       bool any = false;
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
+        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi, add(fj0, (float)(4 * k)));
         act[k] = e < last[k] && !(power > 0.0f || power < B.y);
         cap[k] = false;
         if (may_cap) cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
@@ -170,13 +204,13 @@ __global__ void __launch_bounds__(kBwdThreads, PUV_BWD_MINB) k_raster_bwd(const 
       const double o = d2.y;
       // the thread's pixels share the column px: dx and its terms are computed once, and the
       // dx-only moments follow from the thread's sum of GdL (Mx = dx S, Mxx = dx^2 S)
-      const double dx = d0.x - di, dxx = dx * dx;
+      const double dx = d0.x - di, dxx = dx * dx, dy0 = d0.y - dj0;
       const double hadxx = d1.x * dxx, nbdx = d1.y * dx;
       double gv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // Mx, My, Mxx, Mxy, Myy, sum GdL, colour r, g, b
       double sdy = 0.0;                              // sum GdL dy (-> Mxy = dx sdy)
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const double dy = d0.y - dj[k];
+        const double dy = dy0 - 4.0 * k;
         const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
         double a = act[k] ? o * G : 0.0;
         if (__builtin_expect(may_cap, 0)) a = cap[k] ? 0.99 : a;     // warp-uniform, rare
@@ -199,8 +233,15 @@ __global__ void __launch_bounds__(kBwdThreads, PUV_BWD_MINB) k_raster_bwd(const 
       gv[2] = dxx * gv[5];
       gv[3] = dx * sdy;
       // raw moments into the (view, Gaussian) slot; K7 turns them into dL/d(mx, my, ha, nb, hc)
+#ifndef PUV_BWD_SMEM_RED
+      const double s = warp_reduce9_shfl(gv);
+      double* dst = g2 + 9 * (size_t)sG[j];
+      if ((lane & 3) == 0) atomicAdd(dst + (lane >> 2), s);
+      if (lane == 1) atomicAdd(dst + 8, gv[8]);
+#else
       const double s = warp_sum9(gv, sRed[warp], lane);
       if (lane < 27 && lane % 3 == 0) atomicAdd(g2 + 9 * (size_t)sG[j] + lane / 3, s);
+#endif
     }
   }
 }

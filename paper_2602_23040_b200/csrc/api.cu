@@ -449,6 +449,8 @@ puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_
   StreamSet& ss = stream_set(p.nscratch);
   cudaEventRecord(ss.fork, s);
   for (int i = 0; i < p.nscratch; ++i) cudaStreamWaitEvent(ss.s[i], ss.fork, 0);
+  // Views are composited in groups of kFwdGroup consecutive views per launch (grid.y), each
+  // group once all its views are binned.
   for (int v = 0; v < n_views; ++v) {
     const int i = v % p.nscratch;
     cudaStream_t bs = ss.s[i];
@@ -458,8 +460,11 @@ puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_
     cudaEvent_t done = ss.view_event(v);
     cudaEventRecord(done, bs);
     cudaStreamWaitEvent(s, done, 0);
-    { StageScope sc(PUV_STAGE_RASTER_FWD, s);
-      launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)v * 3 * p.HW, v, bg, s); }
+    const int g0 = v - v % kFwdGroup;
+    if (v == n_views - 1 || (v + 1) % kFwdGroup == 0) {
+      StageScope sc(PUV_STAGE_RASTER_FWD, s);
+      launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)g0 * 3 * p.HW, g0, v + 1 - g0, bg, s);
+    }
   }
   return cuda_check("puv_render_views");
 }

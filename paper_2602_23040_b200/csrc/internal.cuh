@@ -13,6 +13,10 @@ constexpr int kCamBatch = 64;             // views per K1/K7 launch (cameras pas
 constexpr int kTile = PUV_TILE;
 constexpr int kNbMax = 1024;              // max key blocks of the stable tile pass per view
 constexpr int kBinStreams = 4;            // views binned concurrently (one scratch block each)
+#ifndef PUV_FWD_GROUP
+#define PUV_FWD_GROUP 1
+#endif
+constexpr int kFwdGroup = PUV_FWD_GROUP;  // consecutive views per forward-composite launch
 constexpr uint32_t kInvisible = 0xFFFFFFFFu;
 
 struct PlaneTab { const float* p[kMaxPlanes]; };
@@ -105,7 +109,7 @@ void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint
                     cudaStream_t s);
 void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cudaStream_t s);
 void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
-void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* image, int view,
+void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* images, int view0, int n_views,
                        const float bg[3], cudaStream_t s);
 void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int n_views,
                        cudaStream_t s);

@@ -51,9 +51,9 @@ __device__ __forceinline__ bool any_of(const bool (&b)[P]) {
   return r;
 }
 
-__global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, Views v, int view,
+__global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, Views v, int view0,
                                                               int N, int W, int H, int gx, int ntiles, float bg0,
-                                                              float bg1, float bg2, float* __restrict__ image) {
+                                                              float bg1, float bg2, float* __restrict__ images) {
   __shared__ float4 sA[kFwdBatch], sB[kFwdBatch];
   __shared__ double2 sD[5][kFwdBatch];
   __shared__ double sExp[kExpTab];
@@ -63,6 +63,8 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
   const int py0 = ty * kTile + (warp >> 1) * 4 * kFwdPPT + (lane >> 3);
+  const int view = view0 + blockIdx.y;   // grid.y: consecutive views launched together
+  float* image = images + (size_t)blockIdx.y * 3 * W * H;
   const ViewHdr& hdr = v.hdr[view];
   uint32_t start = 0, end = 0;
   if (!hdr.overflow) {
@@ -182,10 +184,12 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
   }
 }
 
-void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* image, int view,
+void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* images, int view0, int n_views,
                        const float bg[3], cudaStream_t s) {
-  k_raster_fwd<<<p.ntiles, kRasterThreads, 0, s>>>(arena, v, view, p.N, p.W, p.H, p.gx, p.ntiles, bg[0], bg[1], bg[2],
-                                                   image);
+  if (n_views <= 0 || p.ntiles <= 0) return;
+  const dim3 grid(p.ntiles, n_views);
+  k_raster_fwd<<<grid, kRasterThreads, 0, s>>>(arena, v, view0, p.N, p.W, p.H, p.gx, p.ntiles, bg[0], bg[1], bg[2],
+                                               images);
   count_launches(1);
 }
 

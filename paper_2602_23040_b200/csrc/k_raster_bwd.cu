@@ -131,18 +131,20 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
   double* g2 = v.grad2d + (size_t)view * N * 9;
   const size_t HW = (size_t)W * H;
   const float* dL_dimage = dL_dimages + (size_t)view * 3 * HW;
-  // pixel k of a thread sits at (px, py0 + 4k): one column, so x-terms are shared and the
-  // row coordinates are formed on the fly (exact: small integers)
-  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-  const int py0 = ty * kTile + (warp >> 1) * 4 * kBwdPPT + (lane >> 3);
-  const float fi = (float)px, fj0 = (float)py0;
-  const double di = px, dj0 = py0;
+  float fi[kBwdPPT], fj[kBwdPPT];
+  double di = 0.0, dj[kBwdPPT];
   uint32_t last[kBwdPPT];
   double dC[kBwdPPT][3], Sd[kBwdPPT], T[kBwdPPT];
   uint32_t tlast = 0;
 #pragma unroll
   for (int k = 0; k < kBwdPPT; ++k) {
-    const int py = py0 + 4 * k;
+    // warp w owns columns 8(w&1).. of rows 4 PPT (w>>1)..; lane l column l&7, rows (l>>3)+4k
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (warp >> 1) * 4 * kBwdPPT + (lane >> 3) + 4 * k;
+    fi[k] = (float)px;
+    fj[k] = (float)py;
+    di = px;   // the same column for every k
+    dj[k] = py;
     last[k] = 0;
     T[k] = 1.0;
     Sd[k] = 0.0;
@@ -192,7 +194,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       bool any = false;
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi, add(fj0, (float)(4 * k)));
+        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
         act[k] = e < last[k] && !(power > 0.0f || power < B.y);
         cap[k] = false;
         if (may_cap) cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
@@ -204,13 +206,28 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       const double o = d2.y;
       // the thread's pixels share the column px: dx and its terms are computed once, and the
       // dx-only moments follow from the thread's sum of GdL (Mx = dx S, Mxx = dx^2 S)
-      const double dx = d0.x - di, dxx = dx * dx, dy0 = d0.y - dj0;
+      const double dx = d0.x - di, dxx = dx * dx;
       const double hadxx = d1.x * dxx, nbdx = d1.y * dx;
       double gv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // Mx, My, Mxx, Mxy, Myy, sum GdL, colour r, g, b
       double sdy = 0.0;                              // sum GdL dy (-> Mxy = dx sdy)
+#ifdef PUV_BWD_KSKIP
+      // pixels k of the warp's lanes form 8x4 sub-blocks: skip a group of PUV_BWD_KSKIP of them
+      // when none of its pixels composites (warp-uniform)
+      unsigned kany = 0;
+#pragma unroll
+      for (int k0 = 0; k0 < kBwdPPT; k0 += PUV_BWD_KSKIP) {
+        bool a = false;
+#pragma unroll
+        for (int k = k0; k < k0 + PUV_BWD_KSKIP; ++k) a |= act[k];
+        kany |= __any_sync(0xffffffffu, a) ? (1u << k0) : 0u;
+      }
+#endif
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-        const double dy = dy0 - 4.0 * k;
+#ifdef PUV_BWD_KSKIP
+        if (!(kany & (1u << (k - k % PUV_BWD_KSKIP)))) continue;
+#endif
+        const double dy = d0.y - dj[k];
         const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
         double a = act[k] ? o * G : 0.0;
         if (__builtin_expect(may_cap, 0)) a = cap[k] ? 0.99 : a;     // warp-uniform, rare

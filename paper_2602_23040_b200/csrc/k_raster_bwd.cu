@@ -210,23 +210,8 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       const double hadxx = d1.x * dxx, nbdx = d1.y * dx;
       double gv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // Mx, My, Mxx, Mxy, Myy, sum GdL, colour r, g, b
       double sdy = 0.0;                              // sum GdL dy (-> Mxy = dx sdy)
-#ifdef PUV_BWD_KSKIP
-      // pixels k of the warp's lanes form 8x4 sub-blocks: skip a group of PUV_BWD_KSKIP of them
-      // when none of its pixels composites (warp-uniform)
-      unsigned kany = 0;
-#pragma unroll
-      for (int k0 = 0; k0 < kBwdPPT; k0 += PUV_BWD_KSKIP) {
-        bool a = false;
-#pragma unroll
-        for (int k = k0; k < k0 + PUV_BWD_KSKIP; ++k) a |= act[k];
-        kany |= __any_sync(0xffffffffu, a) ? (1u << k0) : 0u;
-      }
-#endif
 #pragma unroll
       for (int k = 0; k < kBwdPPT; ++k) {
-#ifdef PUV_BWD_KSKIP
-        if (!(kany & (1u << (k - k % PUV_BWD_KSKIP)))) continue;
-#endif
         const double dy = d0.y - dj[k];
         const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
         double a = act[k] ? o * G : 0.0;

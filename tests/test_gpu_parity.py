@@ -218,6 +218,37 @@ def test_high_opacity_alpha_cap_parity():
     _grad_check(sc, planes, occ, views, dls, grad)
 
 
+def test_binning_dense_overlap_many_segments():
+    """Adversarial binning: 12,000 large Gaussians in front of a 200x136 camera (13 x 9 tiles,
+    ragged), each covering most of the image, so every 4x4-tile super-tile holds ~12k ranks
+    (~24 level-2 segments of 512) and every tile list ~10k entries.  Lists, ranges, visibility,
+    n_contrib, T_final bit-exact; image within tolerance.  Opacities are low (logit ~ N(-3, 0.5)),
+    so pixels composite up to ~11k entries: the backward walks ~175 staged batches per tile and
+    its fp64 T / Sd recurrences run ~11k steps; gradients checked at the north-star tolerance."""
+    rng = np.random.default_rng(5)
+    n = 120 * 100
+    mu = np.stack([rng.uniform(-0.4, 0.4, n), rng.uniform(-0.4, 0.4, n), rng.uniform(-0.3, 0.3, n)], 1)
+    cam = look_at((2.0, 0.0, 0.0), (0.0, 0.0, 0.0), 200, 136, 170.0)
+    sc = tiny_scene(mu, [-1.2] * 3, [1, 0, 0, 0], rng.normal(-3.0, 0.5, n), np.full((n, 3), 0.4), cam, 0)
+    lv = sc.levels[0]
+    lv.planes[3:6] = rng.normal(-1.2, 0.2, (3, 1, n)).astype(np.float32)
+    lv.planes[6:10] = rng.normal(size=(4, 1, n)).astype(np.float32)
+    sc.levels = [Level(planes=np.ascontiguousarray(lv.planes.reshape(-1, 120, 100)),
+                       occ=np.ascontiguousarray(lv.occ.reshape(120, 100)),
+                       labels=np.ascontiguousarray(lv.labels.reshape(120, 100)))]
+    sc.cfg = 97
+    planes, occ, _ = oracle_scene(sc)
+    P = orc.project(planes, occ, cam)
+    vis = P[P["visible"] == 1]
+    assert vis.size > 10000 and vis["tiles"].mean() > 60     # most of the 117 tiles per Gaussian
+    _, dls = _oracle_dls(sc, planes, occ, [0])
+    g, img, loss, grad = _run(sc, [0], dls=dls)
+    _parity_view(sc, g, planes, occ, 0, 0, img[0])
+    dbg = puv.debug_tensors(g["layout"], g["cams"], g["R"].state, g["R"].arena, 0)
+    assert int(dbg["n_contrib"].max().item()) > 5000
+    _grad_check(sc, planes, occ, [0], dls, grad)
+
+
 def test_arena_overflow_flag_and_retry():
     sc = make_scene(1)
     g = gpu_scene(sc, [0], arena_bytes=4096)

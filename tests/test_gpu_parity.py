@@ -249,6 +249,29 @@ def test_binning_dense_overlap_many_segments():
     _grad_check(sc, planes, occ, [0], dls, grad)
 
 
+def test_more_views_than_a_camera_batch():
+    """70 views in one call (> kCamBatch = 64: two K1 / K7 launches, grid.y = 70 in K6): C1's
+    4,096 Gaussians seen from a ring of 70 cameras at 96 x 80 px; every view's binning, pixel state
+    and image, and the 70-view gradient sum, against the oracle."""
+    sc = make_scene(1)
+    cams = []
+    for i in range(70):
+        a = 2 * math.pi * i / 70
+        cams.append(look_at((4 * math.cos(a), 4 * math.sin(a), 0.6 * math.sin(3 * a)), (0, 0, 0), 96, 80, 110.0))
+    sc.cameras = cams
+    sc.cfg = 96
+    views = list(range(70))
+    planes, occ, _ = oracle_scene(sc)
+    _, dls = _oracle_dls(sc, planes, occ, views)
+    g, img, loss, grad = _run(sc, views, dls=dls)
+    for vi in (0, 1, 33, 63, 64, 69):
+        _parity_view(sc, g, planes, occ, vi, vi, img[vi])
+    for vi in views:
+        ref = orc.forward(planes, occ, sc.sh_degree, sc.cameras[vi])[0]
+        assert np.abs(img[vi] - ref).max() <= IMG_ATOL
+    _grad_check(sc, planes, occ, views, dls, grad)
+
+
 def test_arena_overflow_flag_and_retry():
     sc = make_scene(1)
     g = gpu_scene(sc, [0], arena_bytes=4096)

@@ -2,6 +2,7 @@
 //
 // Host runtime only: every step of the path runs in the kernels of this
 // directory.  Argument errors are returned before anything is enqueued.
+#include <nvtx3/nvToolsExt.h>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -38,13 +39,20 @@ static cudaEvent_t take_event() {
   return e;
 }
 
-// RAII: records an event pair around one stage on `s` when profiling is on.
+static const char* const kStageName[] = {"puv:project", "puv:depth_sort", "puv:bin", "puv:raster_fwd",
+                                         "puv:loss", "puv:raster_bwd", "puv:project_bwd", "puv:pack",
+                                         "puv:label", "puv:objective", "puv:quant"};
+
+// RAII: an NVTX range around the host-side enqueue of one stage (for ncu --nvtx filtering and
+// timeline tools; a no-op without a tool attached), and an event pair around the stage on `s`
+// when profiling is on.
 struct StageScope {
   int stage;
   cudaStream_t s;
   cudaEvent_t a = nullptr;
   uint64_t l0 = 0;
   StageScope(int st, cudaStream_t stream) : stage(st), s(stream) {
+    nvtxRangePushA(kStageName[st]);
     if (!g_prof_on) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     a = take_event();
@@ -52,6 +60,7 @@ struct StageScope {
     l0 = g_launches;
   }
   ~StageScope() {
+    nvtxRangePop();
     if (!a) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t b = take_event();

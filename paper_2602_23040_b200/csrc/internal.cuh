@@ -96,6 +96,15 @@ struct Views {
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+// Device-side bounds checks of the data-dependent indexing (arena writes and reads, gids), on in
+// the -DPUV_DEBUG_CHECKS build only (compute-sanitizer is not available on the GPU pool): a
+// violated check traps the kernel, and the call surfaces PUV_E_CUDA.
+#ifdef PUV_DEBUG_CHECKS
+#define PUV_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define PUV_CHECK(cond) do { } while (0)
+#endif
+
 Plan make_plan(const puv_layout& L, int n_views, int W, int H);
 Views views_of(const Plan& p, void* state);
 

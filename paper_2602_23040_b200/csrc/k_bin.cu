@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(kBinThreads) k_tile_scatter(const ViewHdr* hdr
             ml = m - mlo;
           }
           const uint32_t mk = mk_cur[t];
+          PUV_CHECK(cursor[t] + __popc(mk & ((1u << ml) - 1u)) < h.K);
           list[cursor[t] + __popc(mk & ((1u << ml) - 1u))] = sg.gid[mlo + ml];
         }
         __syncthreads();
@@ -598,6 +599,7 @@ __global__ void __launch_bounds__(256) k_seg_walk(const ViewHdr* hdr, const View
   const uint32_t nseg = info->nseg, seglen = info->seglen;
   const int lane = threadIdx.x & 31;
   const uint32_t* list1 = arena + l1->list_base;
+  PUV_CHECK(nseg <= max_segments(gx * gy));
   uint32_t* list = out + hdr->list_base;
   const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < nseg; seg += (gridDim.x * blockDim.x) >> 5) {
@@ -627,7 +629,10 @@ __global__ void __launch_bounds__(256) k_seg_walk(const ViewHdr* hdr, const View
 #pragma unroll
       for (int b = 0; b < kSupT; ++b) {
         const uint32_t bal = __ballot_sync(0xffffffffu, (m >> b) & 1u);
-        if (PASS == 2 && ((m >> b) & 1u)) list[base[b] + __popc(bal & lt)] = cur.z;
+        if (PASS == 2 && ((m >> b) & 1u)) {
+          PUV_CHECK(base[b] + __popc(bal & lt) < hdr->K);
+          list[base[b] + __popc(bal & lt)] = cur.z;
+        }
         base[b] += __popc(bal);
       }
     }

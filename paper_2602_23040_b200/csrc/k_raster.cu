@@ -101,6 +101,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
       const uint32_t idx = b0 + i;
       if (idx < end) {
         const uint32_t g = list[idx];
+        PUV_CHECK(g < (uint32_t)N && idx < hdr.K);
         sA[i] = rec[3 * (size_t)g + 0];
         sB[i] = rec[3 * (size_t)g + 1];
 #pragma unroll

@@ -174,6 +174,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += kBwdThreads) {
       const uint32_t g = list[lo + i];
+      PUV_CHECK(g < (uint32_t)N && start + lo + i < hdr.K);
       sG[i] = g;
       sA[i] = rec[3 * (size_t)g + 0];
       sB[i] = rec[3 * (size_t)g + 1];

@@ -4,6 +4,6 @@ mkdir -p gpurun_out
 C=paper_2602_23040_b200/csrc
 build() {  # name, extra flags, optional replacement source for k_raster_bwd.cu
   if [ -n "${3:-}" ]; then cp $C/k_raster_bwd.cu /tmp/bwd_keep.cu; cp $3 $C/k_raster_bwd.cu; fi
-  touch $C/k_raster*.cu $C/api.cu; make -s -C $C EXTRA="$2" > /tmp/ab_build_$1.log 2>&1; cp paper_2602_23040_b200/libpuv.so /tmp/ab_$1.so
+  touch $C/*.cu; make -s -C $C EXTRA="$2" > /tmp/ab_build_$1.log 2>&1; cp paper_2602_23040_b200/libpuv.so /tmp/ab_$1.so
   if [ -n "${3:-}" ]; then cp /tmp/bwd_keep.cu $C/k_raster_bwd.cu; fi
 }

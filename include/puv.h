@@ -233,6 +233,23 @@ puv_status puv_label_dynamic(const puv_layout* layout, const float* const* atlas
                              int32_t n_cams, const puv_camera* cams, const uint8_t* masks, int32_t r_max,
                              uint8_t* labels, void* workspace, size_t workspace_bytes, void* stream);
 
+/* One fused training step of the L2 harness (steps a1-a9): puv_render_views, then per view
+ * puv_l2_loss_grad and the composite backward, then the projection backward of all views —
+ * the same results as the three calls in sequence (images, T_final, n_contrib and tile lists
+ * bit-identical; loss and gradients up to the order of fp64 atomic additions), but each view's
+ * loss gradient and composite backward run on a second internal stream as soon as the view is
+ * composited, overlapping the compositing and binning of later views.  targets, dL_dimages:
+ * device, like images.  loss: device double, OVERWRITTEN with 1/2 sum (images - targets)^2.
+ * atlas_grad: ACCUMULATED (+=) like puv_render_backward.  On arena overflow the affected views
+ * render nothing and their gradients are not computed (puv_check_overflow, then re-run).
+ * targets_ready: a cudaEvent_t or NULL; the loss gradients wait for it (not the render), so a
+ * host->device copy of the targets recorded on another stream overlaps the render. */
+puv_status puv_render_l2_step(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                              int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, float* images,
+                              const float* targets, float* dL_dimages, double* loss, const uint8_t* dynamic_mask,
+                              void* state, size_t state_bytes, void* arena, size_t arena_bytes,
+                              float* const* atlas_grad, void* targets_ready, void* stream);
+
 /* The one host synchronisation per step: waits for `stream`, then reports
  * whether any view of the last render overflowed the arena and the arena
  * bytes the call needs.  Host outputs. */

@@ -72,16 +72,19 @@ struct StageScope {
 // ---- internal streams for the binning pipeline (one set per device, created on first use) ----
 struct StreamSet {
   cudaStream_t s[kBinStreams] = {};
-  cudaEvent_t fork = nullptr;
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t view_event(int v) {
-    while ((int)ev.size() <= v) {
+  cudaStream_t s2 = nullptr;     // per-view loss + composite backward of the fused L2 step
+  cudaEvent_t fork = nullptr, join = nullptr;
+  std::vector<cudaEvent_t> ev, fev;
+  static cudaEvent_t pooled(std::vector<cudaEvent_t>& pool, int v) {
+    while ((int)pool.size() <= v) {
       cudaEvent_t e;
       cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      ev.push_back(e);
+      pool.push_back(e);
     }
-    return ev[v];
+    return pool[v];
   }
+  cudaEvent_t view_event(int v) { return pooled(ev, v); }
+  cudaEvent_t fwd_event(int v) { return pooled(fev, v); }
 };
 
 static StreamSet& stream_set(int /*n*/) {
@@ -95,6 +98,8 @@ static StreamSet& stream_set(int /*n*/) {
     StreamSet* ss = new StreamSet();
     for (int i = 0; i < kBinStreams; ++i) cudaStreamCreateWithFlags(&ss->s[i], cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&ss->fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss->join, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&ss->s2, cudaStreamNonBlocking);
     sets[dev] = ss;
   }
   return *sets[dev];
@@ -432,16 +437,21 @@ puv_status puv_query_sizes(const puv_layout* layout, int32_t n_views, const puv_
   return PUV_OK;
 }
 
-puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
-                            int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, float* images,
-                            void* state, size_t state_bytes, void* arena, size_t arena_bytes, void* stream) {
-  Common c;
-  puv_status st = prepare(layout, atlas_planes, n_views, cams, opts, state, state_bytes, c);
-  if (st) return st;
-  if (!images) return fail(PUV_E_INVALID_ARGUMENT, "images is NULL");
-  if (!arena && arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "arena is NULL");
-  const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
-  cudaStream_t s = (cudaStream_t)stream;
+// Per-view work the fused L2 step (puv_render_l2_step) attaches to the render pipeline: the loss
+// gradient and the composite backward of view v run on a second compute stream as soon as view
+// v is composited, under the compositing of later views and the binning of the views after them.
+struct L2Hook {
+  const float* targets;
+  float* dL;
+  double* loss;
+  cudaEvent_t targets_ready;   // nullable: the per-view losses wait for it (e.g. an H2D copy of targets)
+};
+
+// Project, bin and composite all views of a call (rows a1-a5); with `hook`, also rows a6-a7 per
+// view.  `s` is ordered after everything enqueued here when the function returns.
+static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_views, const puv_camera* cams,
+                            const float bg[3], float* images, void* state, void* arena, size_t arena_bytes,
+                            cudaStream_t s, const L2Hook* hook) {
   const Plan& p = c.plan;
   cudaMemsetAsync(c.views.hdr, 0, sizeof(ViewHdr) * n_views, s);
   launch_begin_call(p, c.views, arena_bytes / 4, s);
@@ -458,6 +468,10 @@ puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_
   StreamSet& ss = stream_set(p.nscratch);
   cudaEventRecord(ss.fork, s);
   for (int i = 0; i < p.nscratch; ++i) cudaStreamWaitEvent(ss.s[i], ss.fork, 0);
+  if (hook) {
+    cudaStreamWaitEvent(ss.s2, ss.fork, 0);
+    if (hook->targets_ready) cudaStreamWaitEvent(ss.s2, hook->targets_ready, 0);
+  }
   // Views are composited in groups of kFwdGroup consecutive views per launch (grid.y), each
   // group once all its views are binned.
   for (int v = 0; v < n_views; ++v) {
@@ -471,10 +485,38 @@ puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_
     cudaStreamWaitEvent(s, done, 0);
     const int g0 = v - v % kFwdGroup;
     if (v == n_views - 1 || (v + 1) % kFwdGroup == 0) {
-      StageScope sc(PUV_STAGE_RASTER_FWD, s);
-      launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)g0 * 3 * p.HW, g0, v + 1 - g0, bg, s);
+      {
+        StageScope sc(PUV_STAGE_RASTER_FWD, s);
+        launch_raster_fwd(p, c.views, (const uint32_t*)arena, images + (size_t)g0 * 3 * p.HW, g0, v + 1 - g0, bg, s);
+      }
+      if (hook) {
+        cudaEvent_t fdone = ss.fwd_event(v);
+        cudaEventRecord(fdone, s);
+        cudaStreamWaitEvent(ss.s2, fdone, 0);
+        const size_t off = (size_t)g0 * 3 * p.HW, n = (size_t)(v + 1 - g0) * 3 * p.HW;
+        { StageScope sc(PUV_STAGE_LOSS, ss.s2);
+          launch_l2_loss((int64_t)n, images + off, hook->targets + off, hook->dL + off, hook->loss, ss.s2, true); }
+        { StageScope sc(PUV_STAGE_RASTER_BWD, ss.s2);
+          launch_raster_bwd(p, c.views, (const uint32_t*)arena, hook->dL + off, g0, v + 1 - g0, ss.s2); }
+      }
     }
   }
+  if (hook) {
+    cudaEventRecord(ss.join, ss.s2);
+    cudaStreamWaitEvent(s, ss.join, 0);
+  }
+}
+
+puv_status puv_render_views(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                            int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, float* images,
+                            void* state, size_t state_bytes, void* arena, size_t arena_bytes, void* stream) {
+  Common c;
+  puv_status st = prepare(layout, atlas_planes, n_views, cams, opts, state, state_bytes, c);
+  if (st) return st;
+  if (!images) return fail(PUV_E_INVALID_ARGUMENT, "images is NULL");
+  if (!arena && arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "arena is NULL");
+  const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
+  render_pipeline(c, atlas_occ, n_views, cams, bg, images, state, arena, arena_bytes, (cudaStream_t)stream, nullptr);
   return cuda_check("puv_render_views");
 }
 
@@ -483,7 +525,7 @@ puv_status puv_l2_loss_grad(int64_t n, const float* images, const float* targets
   if (n < 0 || (n > 0 && (!images || !targets || !dL_dimages)) || !loss)
     return fail(PUV_E_INVALID_ARGUMENT, "bad loss arguments");
   { StageScope sc(PUV_STAGE_LOSS, (cudaStream_t)stream);
-    launch_l2_loss(n, images, targets, dL_dimages, loss, (cudaStream_t)stream); }
+    launch_l2_loss(n, images, targets, dL_dimages, loss, (cudaStream_t)stream, false); }
   return cuda_check("puv_l2_loss_grad");
 }
 
@@ -580,6 +622,29 @@ puv_status puv_reg_loss_grad(const puv_layout* layout, const float* const* atlas
   return cuda_check("puv_reg_loss_grad");
 }
 
+static puv_status grad_table(const puv_layout* layout, float* const* atlas_grad, GradTab& G) {
+  if (!atlas_grad) return fail(PUV_E_INVALID_ARGUMENT, "atlas_grad is NULL");
+  for (int d = 0; d < layout->planes; ++d) {
+    if (layout->position_mode == PUV_POS_RHO && (d == 1 || d == 2)) { G.p[d] = nullptr; continue; }
+    if (!atlas_grad[d]) return fail(PUV_E_INVALID_ARGUMENT, "grad plane %d is NULL", d);
+    G.p[d] = atlas_grad[d];
+  }
+  return PUV_OK;
+}
+
+// K7 over all views of the call, in camera batches (rows a8, a9)
+static void project_backward(const Common& c, const uint8_t* atlas_occ, int n_views, const puv_camera* cams,
+                             const uint8_t* dynamic_mask, const GradTab& G, cudaStream_t s) {
+  for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
+    CamBatch cb;
+    cb.v0 = v0;
+    cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
+    for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
+    StageScope sc(PUV_STAGE_PROJECT_BWD, s);
+    launch_project_bwd(c.plan, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s);
+  }
+}
+
 puv_status puv_render_backward(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
                                int32_t n_views, const puv_camera* cams, const puv_render_opts* opts,
                                const float* dL_dimages, const uint8_t* dynamic_mask, void* state, size_t state_bytes,
@@ -587,29 +652,38 @@ puv_status puv_render_backward(const puv_layout* layout, const float* const* atl
   Common c;
   puv_status st = prepare(layout, atlas_planes, n_views, cams, opts, state, state_bytes, c);
   if (st) return st;
-  if (!dL_dimages || !atlas_grad) return fail(PUV_E_INVALID_ARGUMENT, "NULL dL_dimages / atlas_grad");
+  if (!dL_dimages) return fail(PUV_E_INVALID_ARGUMENT, "dL_dimages is NULL");
   GradTab G;
-  for (int d = 0; d < layout->planes; ++d) {
-    if (layout->position_mode == PUV_POS_RHO && (d == 1 || d == 2)) { G.p[d] = nullptr; continue; }
-    if (!atlas_grad[d]) return fail(PUV_E_INVALID_ARGUMENT, "grad plane %d is NULL", d);
-    G.p[d] = atlas_grad[d];
-  }
-  const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
+  if ((st = grad_table(layout, atlas_grad, G))) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  const Plan& p = c.plan;
   // all views in one launch (grid = tiles x views): no per-view tail; the background enters
   // through the forward's full colour C
   { StageScope sc(PUV_STAGE_RASTER_BWD, s);
-    launch_raster_bwd(p, c.views, (const uint32_t*)arena, dL_dimages, n_views, s); }
-  for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
-    CamBatch cb;
-    cb.v0 = v0;
-    cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
-    for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
-    StageScope sc(PUV_STAGE_PROJECT_BWD, s);
-    launch_project_bwd(p, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s);
-  }
+    launch_raster_bwd(c.plan, c.views, (const uint32_t*)arena, dL_dimages, 0, n_views, s); }
+  project_backward(c, atlas_occ, n_views, cams, dynamic_mask, G, s);
   return cuda_check("puv_render_backward");
+}
+
+puv_status puv_render_l2_step(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                              int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, float* images,
+                              const float* targets, float* dL_dimages, double* loss, const uint8_t* dynamic_mask,
+                              void* state, size_t state_bytes, void* arena, size_t arena_bytes,
+                              float* const* atlas_grad, void* targets_ready, void* stream) {
+  Common c;
+  puv_status st = prepare(layout, atlas_planes, n_views, cams, opts, state, state_bytes, c);
+  if (st) return st;
+  if (!images || !targets || !dL_dimages || !loss)
+    return fail(PUV_E_INVALID_ARGUMENT, "NULL images / targets / dL_dimages / loss");
+  if (!arena && arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "arena is NULL");
+  GradTab G;
+  if ((st = grad_table(layout, atlas_grad, G))) return st;
+  const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(loss, 0, sizeof(double), s);
+  const L2Hook hook{targets, dL_dimages, loss, (cudaEvent_t)targets_ready};
+  render_pipeline(c, atlas_occ, n_views, cams, bg, images, state, arena, arena_bytes, s, &hook);
+  project_backward(c, atlas_occ, n_views, cams, dynamic_mask, G, s);
+  return cuda_check("puv_render_l2_step");
 }
 
 puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, int32_t* overflowed,

@@ -120,11 +120,12 @@ void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cud
 void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
 void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* images, int view0, int n_views,
                        const float bg[3], cudaStream_t s);
-void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int n_views,
-                       cudaStream_t s);
+void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int view0,
+                       int n_views, cudaStream_t s);
 void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const uint8_t* mask,
                         const CamBatch& cb, const GradTab& G, cudaStream_t s);
-void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s);
+void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s,
+                    bool accumulate);
 void launch_pack(const puv_layout& L, const float* const* level_planes, const uint8_t* const* level_occ,
                  float* const* atlas_planes, uint8_t* atlas_occ, cudaStream_t s);
 void launch_unpack(const puv_layout& L, const float* const* atlas_planes, float* const* level_planes, cudaStream_t s);

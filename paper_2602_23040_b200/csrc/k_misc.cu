@@ -95,8 +95,9 @@ __global__ void __launch_bounds__(256) k_l2_loss(int64_t n, const float* __restr
   }
 }
 
-void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s) {
-  cudaMemsetAsync(loss, 0, sizeof(double), s);
+void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s,
+                    bool accumulate) {
+  if (!accumulate) cudaMemsetAsync(loss, 0, sizeof(double), s);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

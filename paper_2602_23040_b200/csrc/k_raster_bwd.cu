@@ -108,7 +108,7 @@ __device__ __forceinline__ double warp_reduce9_shfl(double (&x)[9]) {
 }
 
 __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, Views v, int N,
-                                                           int W, int H, int gx, int ntiles,
+                                                           int W, int H, int gx, int ntiles, int view0,
                                                            const float* __restrict__ dL_dimages) {
   __shared__ float4 sA[kBwdBatch], sB[kBwdBatch];
   __shared__ double2 sD[5][kBwdBatch];
@@ -119,7 +119,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
 #endif
   __shared__ double sExp[kExpTab];
   exp64_table_fill(sExp);
-  const int tile = blockIdx.x, view = blockIdx.y;
+  const int tile = blockIdx.x, view = view0 + blockIdx.y;   // dL_dimages starts at view0
   const int tx = tile % gx, ty = tile / gx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const ViewHdr& hdr = v.hdr[view];
@@ -130,7 +130,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   double* g2 = v.grad2d + (size_t)view * N * 9;
   const size_t HW = (size_t)W * H;
-  const float* dL_dimage = dL_dimages + (size_t)view * 3 * HW;
+  const float* dL_dimage = dL_dimages + (size_t)blockIdx.y * 3 * HW;
   float fi[kBwdPPT], fj[kBwdPPT];
   double di = 0.0, dj[kBwdPPT];
   uint32_t last[kBwdPPT];
@@ -249,11 +249,11 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
   }
 }
 
-void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int n_views,
-                       cudaStream_t s) {
+void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int view0,
+                       int n_views, cudaStream_t s) {
   if (n_views <= 0 || p.ntiles <= 0) return;
   const dim3 grid(p.ntiles, n_views);
-  k_raster_bwd<<<grid, kBwdThreads, 0, s>>>(arena, v, p.N, p.W, p.H, p.gx, p.ntiles, dL_dimages);
+  k_raster_bwd<<<grid, kBwdThreads, 0, s>>>(arena, v, p.N, p.W, p.H, p.gx, p.ntiles, view0, dL_dimages);
   count_launches(1);
 }
 

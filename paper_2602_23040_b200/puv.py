@@ -92,6 +92,7 @@ def lib():
         L.puv_render_views.argtypes = [P, P, P, S, P, P, P, P, C.c_size_t, P, C.c_size_t, P]
         L.puv_l2_loss_grad.argtypes = [C.c_int64, P, P, P, P, P]
         L.puv_render_backward.argtypes = [P, P, P, S, P, P, P, P, P, C.c_size_t, P, C.c_size_t, P, P]
+        L.puv_render_l2_step.argtypes = [P, P, P, S, P, P, P, P, P, P, P, P, C.c_size_t, P, C.c_size_t, P, P, P]
         L.puv_check_overflow.argtypes = [P, S, P, P, P]
         L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
         L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
@@ -340,6 +341,17 @@ def render_backward(layout, atlas, occ, cams, opts_, dL, mask, state, arena, gra
     _ok(lib().puv_render_backward(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
                                   C.byref(opts_) if opts_ else None, _ptr(dL), _ptr(mask), _ptr(state),
                                   state.numel(), _ptr(arena), arena.numel(), _planes(grad), _stream(stream)))
+
+
+def render_l2_step(layout, atlas, occ, cams, opts_, images, targets, dL, loss, mask, state, arena, grad,
+                   targets_ready=None, stream=None):
+    """Fused render + L2 loss gradient + backward (include/puv.h puv_render_l2_step).
+    targets_ready: optional torch.cuda.Event the loss gradients wait for."""
+    ev = C.c_void_p(targets_ready.cuda_event) if targets_ready is not None else None
+    _ok(lib().puv_render_l2_step(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
+                                 C.byref(opts_) if opts_ else None, _ptr(images), _ptr(targets), _ptr(dL),
+                                 _ptr(loss), _ptr(mask), _ptr(state), state.numel(), _ptr(arena), arena.numel(),
+                                 _planes(grad), ev, _stream(stream)))
 
 
 def label_workspace_bytes(width: int, height: int) -> int:

@@ -42,3 +42,45 @@ def test_step_host_equals_step_c2():
     L_ref = sum(orc.l2_loss_grad(orc.forward(planes, aocc, sc.sh_degree, sc.cameras[v])[0], sc.target(v))[0]
                 for v in st.views)
     assert abs(loss - L_ref) <= 1e-6 * L_ref
+
+
+def test_fused_l2_step_equals_separate_calls_c2():
+    """puv_render_l2_step (per-view loss + composite backward on a second stream, overlapping later
+    views) against render_views + l2_loss_grad + render_backward: images, T_final, n_contrib and the
+    tile lists bit-identical, loss and gradients up to fp64 atomic-order rounding; and the oracle."""
+    sc = make_scene(2, views=6)
+    dev = torch.device("cuda")
+    layout = puv.layout_for_levels([(lv.rows, lv.cols) for lv in sc.levels], sc.sh_degree)
+    atlas, occ = puv.pack_atlas(layout, [torch.from_numpy(lv.planes).to(dev) for lv in sc.levels],
+                                [torch.from_numpy(lv.occ).to(dev) for lv in sc.levels])
+    cams = puv.cameras(sc.cameras)
+    tg = torch.from_numpy(np.stack([sc.target(v) for v in range(6)])).to(dev)
+    R = puv.Renderer(layout, cams, device=dev)
+    img = R.forward(atlas, occ)
+    dL = torch.empty_like(img)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    puv.l2_loss_grad(img, tg, dL, loss)
+    grad = R.backward(atlas, occ, dL)
+    torch.cuda.synchronize()
+    ref = {v: {k: t.clone() for k, t in puv.debug_tensors(layout, cams, R.state, R.arena, v).items()
+               if isinstance(t, torch.Tensor)} for v in range(6)}
+    img_f, dL_f = torch.empty_like(img), torch.empty_like(img)
+    loss_f = torch.zeros(1, dtype=torch.float64, device=dev)
+    grad_f = torch.zeros_like(atlas)
+    for _ in range(2):
+        grad_f.zero_()
+        puv.render_l2_step(layout, atlas, occ, cams, R.opts, img_f, tg, dL_f, loss_f, None, R.state, R.arena, grad_f)
+        torch.cuda.synchronize()
+        assert torch.equal(img_f, img)
+        assert torch.equal(dL_f, dL)
+        assert abs(loss_f.item() - loss.item()) <= 1e-12 * loss.item()
+        for v in range(6):
+            d = puv.debug_tensors(layout, cams, R.state, R.arena, v)
+            for k in ("t_final", "n_contrib", "tile_start", "tile_end", "depth_key", "keys_gid"):
+                assert torch.equal(d[k], ref[v][k]), (v, k)
+        g, r = grad_f.cpu().numpy(), grad.cpu().numpy()
+        assert np.all(np.abs(g - r) <= np.maximum(1e-6 * np.abs(r), GRAD_ATOL))
+    planes, aocc, _ = oracle_scene(sc)
+    L_ref = sum(orc.l2_loss_grad(orc.forward(planes, aocc, sc.sh_degree, sc.cameras[v])[0], sc.target(v))[0]
+                for v in range(6))
+    assert abs(loss_f.item() - L_ref) <= 1e-6 * L_ref

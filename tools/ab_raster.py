@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--views", type=int, default=64)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--tag", default=os.environ.get("PUV_LIB", "default"))
+ap.add_argument("--fused", action="store_true", help="also time the fused puv_render_l2_step")
 a = ap.parse_args()
 sc = make_scene(3, views=a.views)
 dev = torch.device("cuda")
@@ -46,5 +47,25 @@ for _ in range(a.reps):
     torch.cuda.synchronize()
     fw.append(e[0].elapsed_time(e[1]))
     bw.append(e[1].elapsed_time(e[2]))
-print(json.dumps({"tag": a.tag, "views": a.views, "fwd_ms": statistics.median(fw), "bwd_ms": statistics.median(bw),
-                  "fwd_all": fw, "bwd_all": bw}), flush=True)
+sep, fus = [], []
+for _ in range(a.reps):
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    puv.render_views(R.layout, atlas, occ, R.cams, R.opts, img, R.state, R.arena)
+    puv.l2_loss_grad(img, tg, dL, loss)
+    R.backward(atlas, occ, dL, grad=grad)
+    e[1].record()
+    torch.cuda.synchronize()
+    sep.append(e[0].elapsed_time(e[1]))
+    if a.fused:
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record()
+        puv.render_l2_step(R.layout, atlas, occ, R.cams, R.opts, img, tg, dL, loss, None, R.state, R.arena, grad)
+        e[1].record()
+        torch.cuda.synchronize()
+        fus.append(e[0].elapsed_time(e[1]))
+out = {"tag": a.tag, "views": a.views, "fwd_ms": statistics.median(fw), "bwd_ms": statistics.median(bw),
+       "step_sep_ms": statistics.median(sep), "fwd_all": fw, "bwd_all": bw}
+if fus:
+    out["step_fused_ms"] = statistics.median(fus)
+print(json.dumps(out), flush=True)

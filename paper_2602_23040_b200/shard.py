@@ -46,20 +46,24 @@ class ShardedStep:
     def step(self, atlas, occ, targets, grad, mask=None, check_overflow=False):
         """targets: (n_local, 3, H, W) fp32 on device; grad: (D, H_A, W_A) fp32, zeroed by the caller.
         Returns the (device) loss, summed over ranks when world > 1."""
-        if check_overflow:   # sizes the key arena (grow and re-render), then the separate calls
+        # The separate calls, not the fused puv_render_l2_step: the fused pipeline measured the same
+        # step time on C3 (118.7 ms both, the GPU is already saturated by the compositing and the
+        # binning streams), and the separate calls keep each stage alone on its stream, so the
+        # per-stage CUDA-event times the bench reports are not shared with concurrent stages.
+        if check_overflow:   # sizes the key arena (grow and re-render)
             self.R.forward(atlas, occ, images=self.images, check=True)
-            puv.l2_loss_grad(self.images, targets, self.dL, self.loss)
-            self.R.backward(atlas, occ, self.dL, grad=grad, mask=mask)
-        else:                # fused: each view's loss + composite backward overlaps later views
-            puv.render_l2_step(self.R.layout, atlas, occ, self.cams, self.R.opts, self.images, targets, self.dL,
-                               self.loss, mask, self.R.state, self.R.arena, grad)
+        else:
+            puv.render_views(self.R.layout, atlas, occ, self.cams, self.R.opts, self.images, self.R.state,
+                             self.R.arena)
+        puv.l2_loss_grad(self.images, targets, self.dL, self.loss)
+        self.R.backward(atlas, occ, self.dL, grad=grad, mask=mask)
         reduce_gradients(grad, self.loss, self.world, self.group)
         return self.loss
 
     def step_host(self, atlas_host, occ, targets_host, grad, atlas_dev, targets_dev, loss_host, mask=None):
         """The same step from HOST inputs (the end-to-end call): the atlas is copied in first on the
         current stream (K1 reads all of it), the targets on a side copy stream so that their
-        host->device transfer overlaps the render; only the loss gradients wait for them.  The
+        host->device transfer overlaps the render; the loss kernel waits for them.  The
         (rank-summed) loss is read back into `loss_host`.  Host tensors must be pinned for the
         copies to be asynchronous."""
         cur = torch.cuda.current_stream(self.device)
@@ -71,9 +75,11 @@ class ShardedStep:
             targets_dev.copy_(targets_host, non_blocking=True)
             self._targets_ready.record(self._copy_stream)
         atlas_dev.copy_(atlas_host, non_blocking=True)
-        puv.render_l2_step(self.R.layout, atlas_dev, occ, self.cams, self.R.opts, self.images, targets_dev, self.dL,
-                           self.loss, mask, self.R.state, self.R.arena, grad, targets_ready=self._targets_ready)
-        cur.wait_event(self._targets_ready)   # targets_dev stays in use until the step ends
+        puv.render_views(self.R.layout, atlas_dev, occ, self.cams, self.R.opts, self.images, self.R.state,
+                         self.R.arena)
+        cur.wait_event(self._targets_ready)
+        puv.l2_loss_grad(self.images, targets_dev, self.dL, self.loss)
+        self.R.backward(atlas_dev, occ, self.dL, grad=grad, mask=mask)
         reduce_gradients(grad, self.loss, self.world, self.group)
         loss_host.copy_(self.loss, non_blocking=True)
         return loss_host

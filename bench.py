@@ -172,8 +172,8 @@ def stage_work(stage, c, D):
         return "hbm", 8 * nv + 4 * K + 8 * c["ntiles"]
     if stage == "raster_fwd":       # fp64 lane-ops of the value path: 18 per composited pair
         return "alu_fp64", 18 * P
-    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 36
-        return "alu_fp64", 36 * P
+    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 32
+        return "alu_fp64", 32 * P
     if stage == "project_bwd":      # read 2D grads + params, RMW texel grads
         return "hbm", 72 * nv + (D * 4 * 3 * N) / c["views"]
     if stage == "loss":

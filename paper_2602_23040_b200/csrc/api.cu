@@ -218,6 +218,7 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.tfinal = take(4 * V * p.HW);
   p.ncontrib = take(4 * V * p.HW);
   p.cfull = take(24 * V * p.HW);
+  p.dmask = take(32 * V * (size_t)p.ntiles * (size_t)(kMaskCap > 0 ? kMaskCap : 1));
   p.sort_blocks = (N + 2047) / 2048;
   // binning scratch: one block per binning stream; offsets below are relative to a block
   size_t soff = 0;
@@ -253,6 +254,7 @@ Views views_of(const Plan& p, void* state) {
   v.tfinal = (float*)(s + p.tfinal);
   v.ncontrib = (uint32_t*)(s + p.ncontrib);
   v.cfull = (double*)(s + p.cfull);
+  v.dmask = (uint32_t*)(s + p.dmask);
   v.hdr = (ViewHdr*)(s + p.view_hdr);
   v.call = (CallHdr*)(s + p.call_hdr);
   return v;

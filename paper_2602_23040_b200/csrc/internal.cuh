@@ -13,6 +13,16 @@ constexpr int kCamBatch = 64;             // views per K1/K7 launch (cameras pas
 constexpr int kTile = PUV_TILE;
 constexpr int kNbMax = 1024;              // max key blocks of the stable tile pass per view
 constexpr int kBinStreams = 4;            // views binned concurrently (one scratch block each)
+#ifndef PUV_DMASK
+#define PUV_DMASK 1
+#endif
+#ifndef PUV_DMASK_CAP
+#define PUV_DMASK_CAP 384
+#endif
+// K5 records, for the first kMaskCap entries of every tile list, which of the tile's 256 pixels
+// composited the entry (8 words in K6's pixel order); K6 reads the bits instead of replaying the
+// fp32 skip test (entries beyond the cap: replay).  DESIGN.md §6.
+constexpr int kMaskCap = PUV_DMASK ? PUV_DMASK_CAP : 0;
 #ifndef PUV_FWD_GROUP
 #define PUV_FWD_GROUP 1
 #endif
@@ -65,7 +75,7 @@ struct Plan {
   PosMode pm;
   size_t call_hdr, view_hdr;
   // per view arrays, each [n_views][...]
-  size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull;
+  size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull, dmask;
   // scratch shared by all views (reused in stream order)
   // (offsets relative to one scratch block; block i starts at scratch0 + i * scratch_stride)
   size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt, bstart, bin2;
@@ -90,6 +100,7 @@ struct Views {
   float* tfinal;     // [V][HW]
   uint32_t* ncontrib;// [V][HW]
   double* cfull;     // [V][HW][3]  fp64 full colour sum c a T + T_final bg (forward -> backward)
+  uint32_t* dmask;   // [V][ntiles][kMaskCap][8]  composited-pixel bitmask per (tile, entry) (K5 -> K6)
   ViewHdr* hdr;      // [V]
   CallHdr* call;
 };

@@ -92,6 +92,12 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
   }
   // examined pairs of a pixel = entries walked until it terminated (inclusive) or the list ended
   uint32_t exam[kFwdPPT], n_comp = 0;
+  // composited-pixel bits for K6: this warp's two words (K6 order: warp (w & 1), row group
+  // k = 2 (w >> 1) + k') of each of the tile's first kMaskCap entries
+  static_assert(kFwdPPT == 2, "the K6 mask layout assumes 2 pixels per K5 thread");
+  uint2* dmask = kMaskCap > 0 ? reinterpret_cast<uint2*>(v.dmask + ((size_t)view * ntiles + tile) * kMaskCap * 8 +
+                                                          (warp & 1) * 4 + 2 * (warp >> 1))
+                              : nullptr;
 #pragma unroll
   for (int k = 0; k < kFwdPPT; ++k) exam[k] = 0;
   for (uint32_t b0 = start; b0 < end; b0 += kFwdBatch) {
@@ -120,7 +126,12 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         power[k] = pair_power(A.x, A.y, A.z, A.w, B.x, fi, fj[k]);
         hit[k] = !done[k] && !(power[k] > 0.0f || power[k] < B.y);
       }
-      if (!__any_sync(0xffffffffu, any_of(hit))) continue;
+      const uint32_t e = b0 + j - start;   // entry index in the tile list
+      if (!__any_sync(0xffffffffu, any_of(hit))) {
+        if (kMaskCap > 0 && lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(0u, 0u);
+        continue;
+      }
+      bool comp[kFwdPPT] = {};
       // fp64 record and the column terms shared by both pixels (same px): dx, ha dx^2, nb dx
       const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
       const double d4x = sD[4][j].x;
@@ -135,11 +146,12 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         const float Tn = mul(T[k], sub(1.0f, alpha));
         if (Tn < 1e-4f) {
           done[k] = true;
-          exam[k] = b0 + j + 1 - start;
+          exam[k] = e + 1;
           continue;
         }
         T[k] = Tn;
-        last[k] = b0 + j + 1 - start;
+        last[k] = e + 1;
+        comp[k] = true;
         ++n_comp;
         // fp64 value of the composited pair
         const double pw = power64(d2.x, hadxx, nbdx, d0.y - dj[k]);
@@ -149,6 +161,10 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         C[k][1] = fma(d3.y, w, C[k][1]);
         C[k][2] = fma(d4x, w, C[k][2]);
         T64[k] -= w;   // T64 * (1 - a64)
+      }
+      if (kMaskCap > 0) {
+        const uint32_t m0 = __ballot_sync(0xffffffffu, comp[0]), m1 = __ballot_sync(0xffffffffu, comp[1]);
+        if (lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(m0, m1);
       }
       if (__all_sync(0xffffffffu, all_of(done))) break;
     }

@@ -113,6 +113,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
   __shared__ float4 sA[kBwdBatch], sB[kBwdBatch];
   __shared__ double2 sD[5][kBwdBatch];
   __shared__ uint32_t sG[kBwdBatch];
+  __shared__ uint4 sM[kBwdBatch][2];   // K5's composited-pixel words of the staged entries (K6 order)
   __shared__ uint32_t smax[kBwdThreads / 32];
 #ifdef PUV_BWD_SMEM_RED
   __shared__ __align__(16) double sRed[kBwdThreads / 32][kRedRow * 9];
@@ -180,26 +181,53 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       sB[i] = rec[3 * (size_t)g + 1];
 #pragma unroll
       for (int k = 0; k < 5; ++k) sD[k][i] = rec64[5 * (size_t)g + k];
+      if (lo + i < (uint32_t)kMaskCap) {
+        const uint4* m = reinterpret_cast<const uint4*>(v.dmask + (((size_t)view * ntiles + tile) * kMaskCap + lo + i) * 8);
+        sM[i][0] = m[0];
+        sM[i][1] = m[1];
+      }
     }
     __syncthreads();
     for (int j = 0; j < n; ++j) {
       const uint32_t e = lo + j;
       if (e >= wlast) break;  // warp-uniform: no pixel of this warp reaches entry e
-      const float4 A = sA[j], B = sB[j];
-      // decisions (fp32 contract), per pixel.  The cap needs o (x) exp_c(power) >= 0.99 with
-      // power <= 0, where exp_c <= 1 (its last Horner step is 1 + p r with r <= 0, or 2^k <= 1/2),
-      // so an entry with o < 0.99 is never capped: the exp_c replay runs only for the (rare)
-      // entries with o >= 0.99 (warp-uniform branch).
+      const float4 B = sB[j];
+      // decisions (fp32 contract), per pixel: the first kMaskCap entries from K5's composited
+      // bits (bit = composited at this entry; guarded by e < last since K5 writes a warp's words
+      // only until all its pixels terminated), later entries by replaying the skip test.  The cap
+      // needs o (x) exp_c(power) >= 0.99 with power <= 0, where exp_c <= 1 (its last Horner step is
+      // 1 + p r with r <= 0, or 2^k <= 1/2), so an entry with o < 0.99 is never capped: the
+      // exp_c replay runs only for the (rare) entries with o >= 0.99 (warp-uniform branch).
       const bool may_cap = !(B.z < 0.99f);
       bool act[kBwdPPT], cap[kBwdPPT];
       bool any = false;
+      if (e < (uint32_t)kMaskCap) {
+        static_assert(kBwdPPT == 4, "the K5 mask layout assumes 4 pixels per K6 thread");
+        const uint4 mw = sM[j][warp];
+        const uint32_t words[4] = {mw.x, mw.y, mw.z, mw.w};
 #pragma unroll
-      for (int k = 0; k < kBwdPPT; ++k) {
-        const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
-        act[k] = e < last[k] && !(power > 0.0f || power < B.y);
-        cap[k] = false;
-        if (may_cap) cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
-        any |= act[k];
+        for (int k = 0; k < kBwdPPT; ++k) {
+          act[k] = e < last[k] && ((words[k] >> lane) & 1u);
+          any |= act[k];
+        }
+      } else {
+        const float4 A = sA[j];
+#pragma unroll
+        for (int k = 0; k < kBwdPPT; ++k) {
+          const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
+          act[k] = e < last[k] && !(power > 0.0f || power < B.y);
+          any |= act[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kBwdPPT; ++k) cap[k] = false;
+      if (may_cap) {
+        const float4 A = sA[j];
+#pragma unroll
+        for (int k = 0; k < kBwdPPT; ++k) {
+          const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
+          cap[k] = act[k] && !(mul(B.z, exp_c(fminf(power, 0.0f))) < 0.99f);
+        }
       }
       if (!__any_sync(0xffffffffu, any)) continue;
       const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];

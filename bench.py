@@ -170,8 +170,10 @@ def stage_work(stage, c, D):
         return "hbm", 4 * N + 4 * nv
     if stage == "bin":              # read rank rects, write every key once, ranges
         return "hbm", 8 * nv + 4 * K + 8 * c["ntiles"]
-    if stage == "raster_fwd":       # fp64 lane-ops of the value path: 18 per composited pair
-        return "alu_fp64", 18 * P
+    if stage == "raster_fwd":       # fp64-equivalent lane-ops: 18 fp64 per composited pair, plus the
+        # fp32 contract work at half weight (the fp32 pipe is twice as wide): 8 per examined pair (skip
+        # test), 19 per composited pair (exp_c, alpha cap, transmittance, termination test)
+        return "alu_fp64", 18 * P + 0.5 * (8 * E + 19 * P)
     if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 32
         return "alu_fp64", 32 * P
     if stage == "project_bwd":      # read 2D grads + params, RMW texel grads
@@ -326,6 +328,9 @@ def main():
                 "frac": achieved / peak, "traffic": None,
                 "peak_source": f"derived: {nsm} SMs x {lanes} {kind[4:]} lanes x {sm_mhz:.0f} MHz (DESIGN.md §6)"}
     roof["kernel"] = dom
+    roof["work"] = {"raster_fwd": "18 fp64 lane-ops per composited pair + fp32 contract work at half weight "
+                                  "(8 per examined, 19 per composited pair)",
+                    "raster_bwd": "32 fp64 lane-ops per composited pair"}.get(dom, "algorithmic bytes, DESIGN.md §6")
     roof["avg_launch_ms"] = avg_launch_s * 1000.0
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and args.config == 3:

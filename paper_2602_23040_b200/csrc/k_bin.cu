@@ -27,11 +27,23 @@
 
 namespace puv {
 
-constexpr int kBinThreads = 512;
-constexpr int kSG = 256;          // ranks staged per super-group
+#ifndef PUV_BIN_THREADS
+#define PUV_BIN_THREADS 256
+#endif
+#ifndef PUV_BIN_CTAS_PER_SM
+#define PUV_BIN_CTAS_PER_SM 8
+#endif
+constexpr int kBinThreads = PUV_BIN_THREADS;
+constexpr int kSG = kBinThreads < 256 ? kBinThreads : 256;   // ranks staged per super-group
 constexpr int kSub = 32;          // ranks per placement sub-group (mask width)
-constexpr int kItemCache = 2048;  // items of a sub-group whose (tile, member) are cached in smem
-constexpr int kBandTiles = 2048;  // max tiles per band
+#ifndef PUV_BIN_ITEM_CACHE
+#define PUV_BIN_ITEM_CACHE 1024
+#endif
+#ifndef PUV_BIN_BAND_TILES
+#define PUV_BIN_BAND_TILES 512
+#endif
+constexpr int kItemCache = PUV_BIN_ITEM_CACHE;  // items of a sub-group whose (tile, member) are cached in smem
+constexpr int kBandTiles = PUV_BIN_BAND_TILES;  // max tiles per band
 
 __device__ __forceinline__ uint32_t rect_tiles(uint2 r) {
   const uint32_t x0 = r.x & 0xffffu, x1 = r.x >> 16, y0 = r.y & 0xffffu, y1 = r.y >> 16;
@@ -465,7 +477,10 @@ __global__ void __launch_bounds__(kBinThreads) k_tile_scatter(const ViewHdr* hdr
 
 constexpr int kSup = 4;                    // tiles per super-tile side
 constexpr int kSupT = kSup * kSup;         // tiles per super-tile
-constexpr int kSegMin = 512;               // ranks per level-2 segment (at least)
+#ifndef PUV_SEG_MIN
+#define PUV_SEG_MIN 512
+#endif
+constexpr int kSegMin = PUV_SEG_MIN;       // ranks per level-2 segment (at least)
 constexpr int kSegTarget = 32768;          // seglen >= K1 / kSegTarget, so segments <= kSegTarget + nst
 
 __host__ __device__ inline size_t max_segments(int ntiles) { return (size_t)kSegTarget + (size_t)ntiles; }
@@ -718,11 +733,11 @@ void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int
   // level 1: stable counting sort of super-tile keys (ranks) by super-tile
   const int band_rows = sgx >= kBandTiles ? 1 : (kBandTiles / sgx < sgy ? kBandTiles / sgx : sgy);
   const int nbands = (sgy + band_rows - 1) / band_rows;
-  k_tile_count<<<4 * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
+  k_tile_count<<<PUV_BIN_CTAS_PER_SM * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
                                               cnt);
   k_col_scan<<<(nst + 31) / 32, 1024, 0, s>>>(l1, cnt, nst, sen /* totals */);
   k_tile_ranges<<<1, 1024, 0, s>>>(sen, nst, sst, sen);
-  k_tile_scatter<<<4 * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
+  k_tile_scatter<<<PUV_BIN_CTAS_PER_SM * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
                                                 cnt, sst, arena + 0);
   // level 2: per-tile lists from the super-tile rank lists
   k_seg_plan<<<1, 1024, 0, s>>>(l1, sst, sen, nst, segbase, segst, info);

@@ -18,7 +18,10 @@ namespace puv {
 
 constexpr int kOsThreads = 256;
 constexpr int kOsWarps = kOsThreads / 32;
-constexpr int kOsItems = 16;                         // per thread
+#ifndef PUV_OS_ITEMS
+#define PUV_OS_ITEMS 16
+#endif
+constexpr int kOsItems = PUV_OS_ITEMS;               // per thread
 constexpr int kOsTile = kOsThreads * kOsItems;       // 4096 items per CTA
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagPre = 2u << 30, kCountMask = (1u << 30) - 1u;
 

@@ -741,7 +741,10 @@ void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int
                                                 cnt, sst, arena + 0);
   // level 2: per-tile lists from the super-tile rank lists
   k_seg_plan<<<1, 1024, 0, s>>>(l1, sst, sen, nst, segbase, segst, info);
-  const int wblocks = 8 * nsm;   // 8 warps per block, grid-stride over segments
+#ifndef PUV_WALK_CTAS_PER_SM
+#define PUV_WALK_CTAS_PER_SM 8
+#endif
+  const int wblocks = PUV_WALK_CTAS_PER_SM * nsm;   // 8 warps per block, grid-stride over segments
   k_seg_walk<1><<<wblocks, 256, 0, s>>>(hdr, l1, info, segbase, segst, sst, sen, arena, rk, sgx, p.gx, p.gy, cnt2,
                                         nullptr, nullptr);
   k_seg_offsets<<<(nst + 7) / 8, 256, 0, s>>>(l1, segbase, sgx, nst, p.gx, p.gy, cnt2, tend /* totals */);

@@ -12,7 +12,10 @@
 namespace puv {
 
 template <int DEG>
-__global__ void __launch_bounds__(128) k_project(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ, int N,
+#ifndef PUV_PROJ_MINB
+#define PUV_PROJ_MINB 1
+#endif
+__global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ, int N,
                                                  const __grid_constant__ CamBatch cb, Views v, int gx, int gy) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= N) return;

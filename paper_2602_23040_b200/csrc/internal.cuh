@@ -12,7 +12,10 @@ constexpr int kMaxPlanes = 11 + 3 * 16 + 3;   // SH degree 3 + the 3 ray planes 
 constexpr int kCamBatch = 64;             // views per K1/K7 launch (cameras passed by value, 6 KB of params)
 constexpr int kTile = PUV_TILE;
 constexpr int kNbMax = 1024;              // max key blocks of the stable tile pass per view
-constexpr int kBinStreams = 4;            // views binned concurrently (one scratch block each)
+#ifndef PUV_BIN_STREAMS
+#define PUV_BIN_STREAMS 4
+#endif
+constexpr int kBinStreams = PUV_BIN_STREAMS;  // views binned concurrently (one scratch block each)
 #ifndef PUV_DMASK
 #define PUV_DMASK 1
 #endif

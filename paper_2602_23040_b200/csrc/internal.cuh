@@ -13,7 +13,7 @@ constexpr int kCamBatch = 64;             // views per K1/K7 launch (cameras pas
 constexpr int kTile = PUV_TILE;
 constexpr int kNbMax = 1024;              // max key blocks of the stable tile pass per view
 #ifndef PUV_BIN_STREAMS
-#define PUV_BIN_STREAMS 8
+#define PUV_BIN_STREAMS 4
 #endif
 constexpr int kBinStreams = PUV_BIN_STREAMS;  // views binned concurrently (one scratch block each)
 #ifndef PUV_DMASK

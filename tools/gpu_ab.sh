@@ -1,4 +1,6 @@
-# usage: bash tools/gpu_ab.sh  -- builds the variants listed below into /tmp/ab_*.so and times them interleaved
+# A/B helper, sourced by a driver script run through gpurun: `build NAME "FLAGS" [SRC]` compiles libpuv with
+# extra nvcc defines (or a replacement k_raster_bwd.cu) into /tmp/ab_NAME.so; time each with
+#   PUV_LIB=/tmp/ab_NAME.so python tools/ab_raster.py --tag NAME   (interleave builds to cancel box drift)
 set -u
 mkdir -p gpurun_out
 C=paper_2602_23040_b200/csrc

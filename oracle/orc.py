@@ -54,6 +54,8 @@ def lib():
     if _LIB is None:
         L = C.CDLL(build())
         P = C.c_void_p
+        L.orc_set_threads.restype = C.c_int
+        L.orc_set_threads.argtypes = [C.c_int]
         L.orc_exp_c.restype = C.c_float
         L.orc_exp_c.argtypes = [C.c_float]
         L.orc_log_c.restype = C.c_float
@@ -254,6 +256,11 @@ def pack_labels(levels, place, W, H):
 
 # ----------------------------------------------------------------------------
 # projection / binning / render
+
+def set_threads(n: int = 0) -> int:
+    """OpenMP threads of the following oracle calls (n < 1: all host cores); returns the count."""
+    return int(lib().orc_set_threads(int(n)))
+
 
 def project(planes, occ, cam):
     D, H, W = planes.shape

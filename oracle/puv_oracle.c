@@ -34,14 +34,55 @@
  *   atlas layout / pack                                    261-272
  * Everything the paper leaves open follows DESIGN.md §2's readings R1..R16.
  *
- * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared
  *        (x86-64 SSE arithmetic; FLT_EVAL_METHOD == 0).
+ *
+ * Threads (OpenMP, SURVEY.md §8(d) "OpenMP over (view, tile rows)"): projection
+ * and the per-tile sorts run one Gaussian / one tile per iteration; forward and
+ * backward run pixel ROWS round-robin over the threads (schedule(static, 1)).
+ * Every pixel is still computed exactly as written; the only effect is the
+ * order of the backward's per-Gaussian sums: each thread accumulates its rows
+ * into its own buffer and the buffers are added in thread order, so for a given
+ * thread count the result is deterministic.  orc_set_threads(1) gives the plain
+ * single-thread program.
  */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <float.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int orc_nthreads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+static int orc_thread(void)
+{
+#ifdef _OPENMP
+    return omp_get_thread_num();
+#else
+    return 0;
+#endif
+}
+
+/* number of threads of the following calls (n < 1: all host cores); returns the count in use */
+int orc_set_threads(int n)
+{
+#ifdef _OPENMP
+    omp_set_num_threads(n >= 1 ? n : omp_get_num_procs());
+#else
+    (void)n;
+#endif
+    return orc_nthreads();
+}
 
 #if defined(__FLT_EVAL_METHOD__) && __FLT_EVAL_METHOD__ != 0
 #error "oracle needs FLT_EVAL_METHOD == 0 (SSE float arithmetic)"
@@ -296,6 +337,7 @@ static void project_one_f32(const float* const* planes, int64_t g, const orc_cam
 /* planes: D pointers to H_A*W_A floats; occ nullable */
 int orc_project(const float* const* planes, int64_t n, const uint8_t* occ, const orc_camera* cam, orc_proj* out)
 {
+    #pragma omp parallel for schedule(static, 4096)
     for (int64_t g = 0; g < n; ++g) {
         if (occ && !occ[g]) { memset(&out[g], 0, sizeof(orc_proj)); continue; }
         project_one_f32(planes, g, cam, &out[g]);
@@ -349,6 +391,7 @@ int orc_bin(int64_t n, const orc_proj* P, int gx, int gy, uint32_t* start, uint3
                 keys[start[t] + cnt[t]++] = k;
             }
     }
+    #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t t = 0; t < ntiles; ++t)
         qsort(keys + start[t], (size_t)(end[t] - start[t]), sizeof(orc_key), cmp_key);
     for (int64_t i = 0; i < acc; ++i) gids[i] = keys[i].gid;
@@ -519,6 +562,7 @@ static int view_setup(const float* const* dec, const double* const* val, int sh_
     v->end = (uint32_t*)malloc((size_t)nt * 4);
     if (!v->P || !v->VP || !v->start || !v->end) { view_free(v); return -1; }
     orc_project(dec, n, occ, cam, v->P);
+    #pragma omp parallel for schedule(static, 4096)
     for (int64_t g = 0; g < n; ++g)
         if (v->P[g].visible) project_one_f64(val, g, sh_degree, cam, &v->P[g], &v->VP[g], NULL);
     v->K = orc_bin_count(n, v->P);
@@ -541,10 +585,14 @@ int orc_forward(const float* const* dec, const double* const* val, int sh_degree
     int64_t maxlen = 0;
     for (int64_t t = 0; t < (int64_t)v.gx * v.gy; ++t)
         if ((int64_t)(v.end[t] - v.start[t]) > maxlen) maxlen = v.end[t] - v.start[t];
-    comp_entry* ce = (comp_entry*)malloc((size_t)(maxlen > 0 ? maxlen : 1) * sizeof(comp_entry));
-    if (!ce) { view_free(&v); return -1; }
+    if (maxlen < 1) maxlen = 1;
+    const int nthr = orc_nthreads();
+    comp_entry* ce_all = (comp_entry*)malloc((size_t)nthr * (size_t)maxlen * sizeof(comp_entry));
+    if (!ce_all) { view_free(&v); return -1; }
     int64_t composited = 0;
-    for (int j = 0; j < H; ++j)
+    #pragma omp parallel for schedule(static, 1) reduction(+ : composited)
+    for (int j = 0; j < H; ++j) {
+        comp_entry* ce = ce_all + (size_t)orc_thread() * (size_t)maxlen;
         for (int i = 0; i < W; ++i) {
             int64_t t = (int64_t)(j / ORC_TILE) * v.gx + (i / ORC_TILE);
             int32_t nctr; float T32;
@@ -561,12 +609,13 @@ int orc_forward(const float* const* dec, const double* const* val, int sh_degree
             if (ncontrib_out) ncontrib_out[(int64_t)j * W + i] = nctr;
             composited += nc;
         }
+    }
     if (stats) {
         int64_t nvis = 0;
         for (int64_t g = 0; g < n; ++g) nvis += v.P[g].visible;
         stats[0] = nvis; stats[1] = v.K; stats[2] = composited;
     }
-    free(ce);
+    free(ce_all);
     view_free(&v);
     return 0;
 }
@@ -584,12 +633,17 @@ int orc_backward(const float* const* dec, const double* const* val, int sh_degre
     int64_t maxlen = 0;
     for (int64_t t = 0; t < (int64_t)v.gx * v.gy; ++t)
         if ((int64_t)(v.end[t] - v.start[t]) > maxlen) maxlen = v.end[t] - v.start[t];
-    comp_entry* ce = (comp_entry*)malloc((size_t)(maxlen > 0 ? maxlen : 1) * sizeof(comp_entry));
-    /* per-Gaussian 2D gradients: mx, my, ha, nb, hc, o, r, g, b */
-    double* g2 = (double*)calloc((size_t)n * 9, sizeof(double));
-    if (!ce || !g2) { free(ce); free(g2); view_free(&v); return -1; }
+    if (maxlen < 1) maxlen = 1;
+    const int nthr = orc_nthreads();
+    comp_entry* ce_all = (comp_entry*)malloc((size_t)nthr * (size_t)maxlen * sizeof(comp_entry));
+    /* per-Gaussian 2D gradients: mx, my, ha, nb, hc, o, r, g, b; one buffer per thread */
+    double* g2_all = (double*)calloc((size_t)nthr * (size_t)n * 9, sizeof(double));
+    if (!ce_all || !g2_all) { free(ce_all); free(g2_all); view_free(&v); return -1; }
 
-    for (int j = 0; j < H; ++j)
+    #pragma omp parallel for schedule(static, 1)
+    for (int j = 0; j < H; ++j) {
+        comp_entry* ce = ce_all + (size_t)orc_thread() * (size_t)maxlen;
+        double* g2 = g2_all + (size_t)orc_thread() * (size_t)n * 9;
         for (int i = 0; i < W; ++i) {
             int64_t t = (int64_t)(j / ORC_TILE) * v.gx + (i / ORC_TILE);
             int32_t nctr; float T32;
@@ -622,10 +676,17 @@ int orc_backward(const float* const* dec, const double* const* val, int sh_degre
                 g2[g * 9 + 1] += (B->nb * dx + 2.0 * B->hc * dy) * dP;
             }
         }
+    }
+    /* thread buffers summed in thread order into buffer 0 */
+    double* g2 = g2_all;
+    #pragma omp parallel for schedule(static, 4096)
+    for (int64_t q = 0; q < n * 9; ++q)
+        for (int t = 1; t < nthr; ++t) g2[q] += g2_all[(size_t)t * (size_t)n * 9 + (size_t)q];
 
-    /* per-Gaussian chain rule to texel planes (DESIGN.md §1 backward) */
+    /* per-Gaussian chain rule to texel planes (DESIGN.md §1 backward); each g writes only its own texel */
     int nk = (sh_degree + 1) * (sh_degree + 1);
     const float* V = cam->viewmat;
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t g = 0; g < n; ++g) {
         if (!v.P[g].visible) continue;
         const double* d2 = g2 + g * 9;
@@ -715,7 +776,7 @@ int orc_backward(const float* const* dec, const double* const* val, int sh_degre
         for (int k = 0; k < 4; ++k) grad[6 + k][g] += scale * dqraw[k];
         grad[10][g] += scale * d2[5] * X.o * (1.0 - X.o);
     }
-    free(ce); free(g2);
+    free(ce_all); free(g2_all);
     view_free(&v);
     return 0;
 }

@@ -20,6 +20,10 @@
  *    are asynchronous: argument errors are returned synchronously before any
  *    work is enqueued; CUDA launch errors surface as PUV_E_CUDA.
  *  - After an error, puv_last_error() returns a thread-local message.
+ *  - Thread safety: calls may come from several host threads, also on one
+ *    device (the library's internal binning streams are shared per device and
+ *    their enqueue is serialised by a lock); two calls must not share a state
+ *    or arena buffer concurrently.
  *  - Texel planes are fp32, SoA: plane d of an atlas is H_A*W_A floats, row
  *    major; texel id (gid) = y*W_A + x.  Plane order (R2):
  *      [x, y, z, ls0, ls1, ls2, qw, qx, qy, qz, logit_o, sh(k,c) at 11+3k+c]
@@ -213,7 +217,9 @@ puv_status puv_quantize(const puv_layout* layout, const float* const* atlas_plan
 /* Backward of the last puv_render_views with the same layout/cams/opts/state/arena
  * (steps a7-a9).  dL_dimages: device, like images.  dynamic_mask: device
  * H_A*W_A bytes (D_i of PAPER.md:410-414) or NULL.  atlas_grad: host array of D
- * device pointers; gradients w.r.t. the texel planes are ACCUMULATED (+=). */
+ * device pointers; gradients w.r.t. the texel planes are ACCUMULATED (+=).
+ * Re-entrant: the per-(view, Gaussian) moment slots in `state` are reset by every call, so k
+ * calls after one render add k times the gradient (e.g. two loss terms on one forward). */
 puv_status puv_render_backward(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
                                int32_t n_views, const puv_camera* cams, const puv_render_opts* opts,
                                const float* dL_dimages, const uint8_t* dynamic_mask, void* state, size_t state_bytes,

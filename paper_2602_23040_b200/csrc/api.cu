@@ -70,7 +70,11 @@ struct StageScope {
 };
 
 // ---- internal streams for the binning pipeline (one set per device, created on first use) ----
+// One set per device, shared by every call on that device: `mu` serialises the enqueue of a
+// render pipeline (the growable event pools and the fork/join events are not thread-safe), so
+// host threads may call the library concurrently on one device.
 struct StreamSet {
+  std::mutex mu;
   cudaStream_t s[kBinStreams] = {};
   cudaStream_t s2 = nullptr;     // per-view loss + composite backward of the fused L2 step
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -468,6 +472,7 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
   // Pipeline: view v is depth-sorted and binned on binning stream v % nscratch (its own scratch
   // block) while earlier views composite on `s`; `s` waits on view v's binning event only.
   StreamSet& ss = stream_set(p.nscratch);
+  std::lock_guard<std::mutex> lock(ss.mu);
   cudaEventRecord(ss.fork, s);
   for (int i = 0; i < p.nscratch; ++i) cudaStreamWaitEvent(ss.s[i], ss.fork, 0);
   if (hook) {
@@ -658,6 +663,9 @@ puv_status puv_render_backward(const puv_layout* layout, const float* const* atl
   GradTab G;
   if ((st = grad_table(layout, atlas_grad, G))) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  // the (view, Gaussian) moment slots K6 accumulates into start at zero on every backward call,
+  // so backward can be called repeatedly on one forward state (each call adds its gradient once)
+  cudaMemsetAsync(c.views.grad2d, 0, (size_t)72 * n_views * c.plan.N, s);
   // all views in one launch (grid = tiles x views): no per-view tail; the background enters
   // through the forward's full colour C
   { StageScope sc(PUV_STAGE_RASTER_BWD, s);
@@ -682,6 +690,7 @@ puv_status puv_render_l2_step(const puv_layout* layout, const float* const* atla
   const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
   cudaStream_t s = (cudaStream_t)stream;
   cudaMemsetAsync(loss, 0, sizeof(double), s);
+  cudaMemsetAsync(c.views.grad2d, 0, (size_t)72 * n_views * c.plan.N, s);   // K6's moment slots
   const L2Hook hook{targets, dL_dimages, loss, (cudaEvent_t)targets_ready};
   render_pipeline(c, atlas_occ, n_views, cams, bg, images, state, arena, arena_bytes, s, &hook);
   project_backward(c, atlas_occ, n_views, cams, dynamic_mask, G, s);

@@ -5,8 +5,8 @@
 // it writes: the depth key and tile rect (fp32 contract, R13 -> binning), the
 // 48-byte fp32 record (contract conic/mean/t_g/o + colour -> forward raster and
 // every compositing decision) and the 80-byte fp64 value record (the same
-// quantities in double -> backward).  It also zeroes the
-// (view, Gaussian) 2D-gradient slot that K6 accumulates into.
+// quantities in double -> backward).  The (view, Gaussian) 2D-gradient slots
+// K6 accumulates into are zeroed by the backward call itself (re-entrant backward).
 #include "project.cuh"
 
 namespace puv {
@@ -82,9 +82,6 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
     r64[2] = make_double2(p64.hc, u64.o);
     r64[3] = make_double2(rgb[0], rgb[1]);
     r64[4] = make_double2(rgb[2], 0.0);
-    double* g2 = v.grad2d + 9 * o;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) g2[k] = 0.0;
   }
 }
 

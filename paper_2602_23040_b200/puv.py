@@ -263,13 +263,34 @@ def query_sizes(layout: Layout, cams, opts_=None):
     return sb.value, ah.value
 
 
+def _check_images(name, t, n_views, cams, dtype=torch.float32):
+    """Image-like argument: contiguous CUDA tensor of `dtype` with n_views*3*H*W elements (the C ABI
+    reads and writes that many elements at its data pointer)."""
+    W, H = cams[0].width, cams[0].height
+    assert isinstance(t, torch.Tensor) and t.is_cuda, f"{name}: CUDA tensor expected"
+    assert t.dtype == dtype, f"{name}: {dtype} expected, got {t.dtype}"
+    assert t.is_contiguous(), f"{name}: must be contiguous"
+    assert t.numel() == n_views * 3 * H * W, f"{name}: {t.numel()} elements != n_views*3*H*W = {n_views * 3 * H * W}"
+
+
+def _check_loss(loss):
+    assert isinstance(loss, torch.Tensor) and loss.is_cuda and loss.dtype == torch.float64 and loss.numel() >= 1, \
+        "loss: CUDA fp64 tensor with >= 1 element expected"
+
+
 def render_views(layout, atlas, occ, cams, opts_, images, state, arena, stream=None):
+    _check_images("images", images, len(cams), cams)
     _ok(lib().puv_render_views(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
                                C.byref(opts_) if opts_ else None, _ptr(images), _ptr(state), state.numel(),
                                _ptr(arena), arena.numel(), _stream(stream)))
 
 
 def l2_loss_grad(images, targets, dL, loss, stream=None):
+    for name, t in (("images", images), ("targets", targets), ("dL", dL)):
+        assert isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous(), \
+            f"{name}: contiguous fp32 CUDA tensor expected"
+        assert t.numel() == images.numel(), f"{name}: {t.numel()} elements != images' {images.numel()}"
+    _check_loss(loss)
     _ok(lib().puv_l2_loss_grad(images.numel(), _ptr(images), _ptr(targets), _ptr(dL), _ptr(loss), _stream(stream)))
 
 
@@ -314,6 +335,11 @@ def photo_loss_grad(images, targets, dL, loss, lambda_ssim=0.2, workspace=None, 
     """L1 + SSIM photometric loss (PAPER.md:449-452).  images/targets/dL: (V, 3, H, W) fp32 CUDA;
     loss: (1,) fp64 CUDA, overwritten.  Returns the workspace (reuse it across calls)."""
     V, _, H, W = images.shape
+    for name, t in (("images", images), ("targets", targets), ("dL", dL)):
+        assert isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous(), \
+            f"{name}: contiguous fp32 CUDA tensor expected"
+        assert tuple(t.shape) == (V, 3, H, W), f"{name}: shape {tuple(t.shape)} != {(V, 3, H, W)}"
+    _check_loss(loss)
     if workspace is None:
         workspace = torch.empty(photo_workspace_bytes(W, H, min(V, 8)), dtype=torch.uint8, device=images.device)
     _ok(lib().puv_photo_loss_grad(V, W, H, _ptr(images), _ptr(targets), float(lambda_ssim), _ptr(dL), _ptr(loss),
@@ -338,6 +364,7 @@ def reg_loss_grad(layout, atlas, occ, grad, loss, lambda_scale=1e-4, lambda_opac
 
 
 def render_backward(layout, atlas, occ, cams, opts_, dL, mask, state, arena, grad, stream=None):
+    _check_images("dL", dL, len(cams), cams)
     _ok(lib().puv_render_backward(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
                                   C.byref(opts_) if opts_ else None, _ptr(dL), _ptr(mask), _ptr(state),
                                   state.numel(), _ptr(arena), arena.numel(), _planes(grad), _stream(stream)))
@@ -348,6 +375,9 @@ def render_l2_step(layout, atlas, occ, cams, opts_, images, targets, dL, loss, m
     """Fused render + L2 loss gradient + backward (include/puv.h puv_render_l2_step).
     targets_ready: optional torch.cuda.Event the loss gradients wait for."""
     ev = C.c_void_p(targets_ready.cuda_event) if targets_ready is not None else None
+    for name, t in (("images", images), ("targets", targets), ("dL", dL)):
+        _check_images(name, t, len(cams), cams)
+    _check_loss(loss)
     _ok(lib().puv_render_l2_step(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams,
                                  C.byref(opts_) if opts_ else None, _ptr(images), _ptr(targets), _ptr(dL),
                                  _ptr(loss), _ptr(mask), _ptr(state), state.numel(), _ptr(arena), arena.numel(),

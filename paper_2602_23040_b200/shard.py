@@ -43,9 +43,15 @@ class ShardedStep:
         self.dL = torch.empty_like(self.images)
         self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
 
-    def step(self, atlas, occ, targets, grad, mask=None, check_overflow=False):
+    def step(self, atlas, occ, targets, grad, mask=None, check_overflow=True):
         """targets: (n_local, 3, H, W) fp32 on device; grad: (D, H_A, W_A) fp32, zeroed by the caller.
-        Returns the (device) loss, summed over ranks when world > 1."""
+        Returns the (device) loss, summed over ranks when world > 1.
+
+        check_overflow (default on): after the forward, read the key-arena overflow flag (one host
+        sync) and, if a view did not fit, grow the arena and re-render before the loss and the
+        backward, so an overflowed view can never contribute a wrong gradient.  Callers that have
+        sized the arena already (the bench, after its first warm-up step) opt out explicitly and
+        check `overflowed()` after their timed region."""
         # The separate calls, not the fused puv_render_l2_step: the fused pipeline measured the same
         # step time on C3 (118.7 ms both, the GPU is already saturated by the compositing and the
         # binning streams), and the separate calls keep each stage alone on its stream, so the

@@ -6,6 +6,9 @@ formed, the backward scatters gradients onto the atlas texels, and (N > 1) the
 gradient planes are all-reduced over NCCL.  Default workload: BJ.configs[2]
 (C3: 1,048,576 Gaussians, SH degree 3, 64 views at 1920x1080), all 64 views per
 step (strong scaling over N GPUs: rank r renders views r, r+N, ...).
+--config 4: the C4 frame sequence (30 frames x 55 views = 1650 view-renders per
+step, gradient freezing); --config 5: C5 (5.24M Gaussians, 88 views at 4K, in
+view chunks that fit HBM).
 
     python bench.py [--gpus N --steps K --warmup W] [--config 3] [--impl reference]
 
@@ -16,7 +19,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -32,7 +34,10 @@ METRIC = "views/sec fwd+bwd render of UV-atlas Gaussians @1080p, 1/2/4/8 GPUs"
 UNIT = "views/s"
 WORKLOADS = {1: "BJ.configs[0] C1: 64x64 atlas (4096 G, SH0), 1 view 128x128",
              2: "BJ.configs[1] C2: 512^2+256^2+128^2 levels (344,064 G, SH1), 16 views 1024x768",
-             3: "BJ.configs[2] C3: 1024^2 atlas (1,048,576 G, SH3), 64 views 1920x1080"}
+             3: "BJ.configs[2] C3: 1024^2 atlas (1,048,576 G, SH3), 64 views 1920x1080",
+             4: "BJ.configs[3] C4: 30 frames of a 1024^2 atlas (SH3, 25% dynamic texels, gradient freezing), "
+                "55 views 1920x1080: 1650 view-renders per step",
+             5: "BJ.configs[4] C5: 2048^2+1024^2 levels (5,242,880 G, SH3), 88 views 3840x2160"}
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                  0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                  0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
@@ -45,10 +50,13 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--views", type=int, default=None, help="use only the first V views of the config")
+    ap.add_argument("--frames", type=int, default=None, help="C4: use only the first F frames")
+    ap.add_argument("--views-per-call", type=int, default=None, help="view chunk of one render call")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-views", type=int, default=1)
+    ap.add_argument("--no-serial", action="store_true", help="skip the serialised per-stage profile step")
+    ap.add_argument("--cpu-sample-views", type=int, default=2)
     return ap.parse_args()
 
 
@@ -105,51 +113,65 @@ class ClockSampler:
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 
 
-def oracle_views_per_s(scene, views, targets=None):
-    """Time the CPU oracle (as it stands) doing fwd+bwd of `views`; returns (views/s, seconds, cores)."""
+def host_cpu():
+    model = "unknown"
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
+
+
+def oracle_views_per_s(scene, views, threads=0):
+    """Time the CPU oracle (as it stands) doing fwd+bwd of `views` with `threads` OpenMP threads
+    (0 = all host cores); returns (views/s, seconds, threads used)."""
     from oracle import orc
     planes, occ, _ = orc.pack(scene.levels)
+    val = planes.astype(np.float64)
+    used = orc.set_threads(threads)
     t0 = time.perf_counter()
     for v in views:
         cam = scene.cameras[v]
-        img = orc.forward(planes, occ, scene.sh_degree, cam)[0]
-        tg = scene.target(v) if targets is None else targets[v]
-        _, dl = orc.l2_loss_grad(img, tg)
-        orc.backward(planes, occ, scene.sh_degree, cam, dl)
+        img = orc.forward(planes, occ, scene.sh_degree, cam, val=val)[0]
+        _, dl = orc.l2_loss_grad(img, scene.target(v))
+        orc.backward(planes, occ, scene.sh_degree, cam, dl, val=val)
     dt = time.perf_counter() - t0
-    return len(views) / dt, dt, 1
+    orc.set_threads(0)
+    return len(views) / dt, dt, used
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle is this tier's reference arm (runs on rank 0 only)."""
+    """--impl reference: the CPU oracle (all host cores) is this tier's reference arm (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from synth.scenes import make_scene
-    sc = make_scene(args.config, views=args.views)
-    nv = max(1, args.cpu_sample_views)
-    sample = list(range(nv))
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up effects worth paying minutes for; see DESIGN.md §6
-    times = []
+    cfg = args.config if args.config != 4 else 3   # C4 frames are C3-sized atlases; sample on C3's views
+    sc = make_scene(cfg, views=args.views)
+    nv = 1   # one full-resolution view fwd+bwd per step keeps the driver's 20-step run to minutes
+    times, used = [], 0
     for s in range(args.steps):
-        vps, dt, cores = oracle_views_per_s(sc, [sample[s % nv]])
+        _, dt, used = oracle_views_per_s(sc, [(s * nv + i) % len(sc.cameras) for i in range(nv)])
         times.append(dt)
     t = sum(times) / len(times)
-    value = 1.0 / t
+    value = nv / t
+    hc = host_cpu()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS.get(args.config, str(args.config)), "views_per_step": 1,
-                       "parallelism": "single CPU thread (oracle)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"1 view (of {len(sc.cameras)}) fwd+bwd per step, full resolution"},
+            "config": {"workload": WORKLOADS.get(args.config, str(args.config)), "views_per_step": nv,
+                       "parallelism": f"CPU oracle, OpenMP over pixel rows on {used} threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle",
+                             "sample": f"{nv} view(s) (of {len(sc.cameras)}) fwd+bwd per step, full resolution",
+                             **hc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------------------------
-# roofline bookkeeping (DESIGN.md §6: algorithmic work per unit)
+# roofline bookkeeping (DESIGN.md §6 / SURVEY.md §8(d): algorithmic work per unit)
 
 
 def load_peaks():
@@ -161,26 +183,66 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
 
 
+# SURVEY.md §8(d) FP32-pipe instruction counts of the compositing kernels (per (pixel, entry) pair)
+K5_PER_EXAMINED, K5_PER_COMPOSITED = 8, 11
+K6_PER_EXAMINED, K6_PER_COMPOSITED = 8, 45
+
+
 def stage_work(stage, c, D):
-    """Algorithmic work of ONE launch-set of `stage` for the per-view counts c."""
+    """Algorithmic work of the per-view share of `stage` for the per-view counts c:
+    ('hbm', bytes) or ('alu_fp32', FP32 lane-instructions)."""
     N, nv, K, E, P = c["N"], c["n_vis"], c["K"], c["examined"], c["composited"]
-    if stage == "project":          # per view share of K1: texel read (once per call) + records written
-        return "hbm", (D * 4 * N) / c["views"] + 212 * nv + 4 * (N - nv)
+    sh = 4 * (D - 11)
+    if stage == "project":          # SURVEY §8(d): 44 B geometry + SH of a visible G, ~56 B record out
+        return "hbm", 44 * N / c["views"] + (sh + 56) * nv
     if stage == "depth_sort":       # read the depth key of every texel, write the depth order
         return "hbm", 4 * N + 4 * nv
-    if stage == "bin":              # read rank rects, write every key once, ranges
-        return "hbm", 8 * nv + 4 * K + 8 * c["ntiles"]
-    if stage == "raster_fwd":       # fp64-equivalent lane-ops (DESIGN.md §6): 18 fp64 per composited pair, plus the
-        # fp32 contract work at half weight (the fp32 pipe is twice as wide): 8 per examined pair (skip
-        # test), 19 per composited pair (exp_c, alpha cap, transmittance, termination test)
-        return "alu_fp64", 18 * P + 0.5 * (8 * E + 19 * P)
-    if stage == "raster_bwd":       # fp64 lane-ops per composited pair: 32 (DESIGN.md §6)
-        return "alu_fp64", 32 * P
-    if stage == "project_bwd":      # read 2D grads + params, RMW texel grads
-        return "hbm", 72 * nv + (D * 4 * 3 * N) / c["views"]
+    if stage == "bin":              # SURVEY §8(d): 12 B per key written (+ rank rects, ranges)
+        return "hbm", 8 * nv + 12 * K + 8 * c["ntiles"]
+    if stage == "raster_fwd":       # SURVEY §8(d): 8 FP32 instr per examined pair, +11 per composited pair
+        return "alu_fp32", K5_PER_EXAMINED * E + K5_PER_COMPOSITED * P
+    if stage == "raster_bwd":       # SURVEY §8(d): ~8 per evaluated pair, ~45 per composited pair
+        return "alu_fp32", K6_PER_EXAMINED * E + K6_PER_COMPOSITED * P
+    if stage == "project_bwd":      # 9 moments + params read per visible G, texel gradient RMW once per call
+        return "hbm", (72 + 44 + sh) * nv + (D * 4 * 2 * N) / c["views"]
     if stage == "loss":
         return "hbm", 12 * 3 * c["HW"]
     return "hbm", 0
+
+
+def roofline(stage, per_view, D, views_in_stage, stage_ms, calls, peaks, nsm, fp64_secondary=True):
+    kind, work = stage_work(stage, per_view, D)
+    avg_launch_s = stage_ms / 1000.0 / max(calls, 1)
+    work_per_launch = work * views_in_stage / max(calls, 1)
+    if kind == "hbm":
+        achieved = work_per_launch / avg_launch_s / 1e9
+        r = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+             "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"]}
+    else:
+        peak = nsm * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12
+        achieved = work_per_launch / avg_launch_s / 1e12
+        r = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T FP32 lane-instr/s",
+             "frac": achieved / peak, "traffic": None,
+             "peak_source": f"derived: {nsm} SMs x 128 FP32 lanes x {peaks['sm_max_mhz']:.0f} MHz "
+                            "(B200_PROFILING.md unit counts; DESIGN.md §6)",
+             "work": {"raster_fwd": f"SURVEY §8(d): {K5_PER_EXAMINED} FP32 instr per examined (pixel, entry) pair "
+                                    f"+ {K5_PER_COMPOSITED} per composited pair",
+                      "raster_bwd": f"SURVEY §8(d): {K6_PER_EXAMINED} per examined + {K6_PER_COMPOSITED} per "
+                                    "composited pair"}[stage]}
+        if fp64_secondary:
+            # the build's own value path (DESIGN.md §5): fp64 lane-ops per composited pair vs 64 FP64 lanes/SM
+            n64 = {"raster_fwd": 18, "raster_bwd": 32}[stage] * per_view["composited"] * views_in_stage / max(calls, 1)
+            p64 = nsm * 64 * peaks["sm_max_mhz"] * 1e6 / 1e12
+            r["fp64_value_path"] = {"achieved": n64 / avg_launch_s / 1e12, "peak": p64,
+                                    "frac": n64 / avg_launch_s / 1e12 / p64, "unit": "T FP64 lane-ops/s",
+                                    "work": f"{ {'raster_fwd': 18, 'raster_bwd': 32}[stage]} fp64 ops per "
+                                            "composited pair (DESIGN.md §6)"}
+    r["kernel"] = stage
+    r["avg_launch_ms"] = avg_launch_s * 1000.0
+    return r
+
+
+# ----------------------------------------------------------------------------------------------
 
 
 def main():
@@ -192,42 +254,81 @@ def main():
     import torch.distributed as dist
 
     from paper_2602_23040_b200 import puv
-    from paper_2602_23040_b200.shard import ShardedStep
-    from synth.scenes import make_scene
+    from paper_2602_23040_b200.shard import FrameStep, ShardedStep
+    from synth.scenes import frame_positions, make_scene
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one process per GPU)")
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one process per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     puv.lib()
 
-    sc = make_scene(args.config, views=args.views)
+    cfg = args.config
+    sc = make_scene(cfg, views=args.views)
     n_views = len(sc.cameras)
     layout = puv.layout_for_levels([(lv.rows, lv.cols) for lv in sc.levels], sc.sh_degree)
     lp = [torch.from_numpy(lv.planes).to(dev) for lv in sc.levels]
     lo = [torch.from_numpy(lv.occ).to(dev) for lv in sc.levels]
     atlas, occ = puv.pack_atlas(layout, lp, lo)
     del lp, lo
-    stepper = ShardedStep(layout, sc.cameras, rank, world, dev)
-    mine = stepper.views
-    tg_host = torch.from_numpy(np.stack([sc.target(v) for v in mine])).pin_memory()
-    targets = tg_host.to(dev)
-    grad = torch.zeros_like(atlas)
+    D = layout.planes
+    N = layout.atlas_w * layout.atlas_h
+    W, H = sc.cameras[0].width, sc.cameras[0].height
+
+    vpc = args.views_per_call
+    if vpc is None and cfg == 5:
+        # C5 does not fit one call at 88 views: chunk so that state + key arena use
+        # about half of the free HBM (arena estimate: 1.3 x the library's first guess per view)
+        free = torch.cuda.mem_get_info(dev)[0]
+        sb1, ah1 = puv.query_sizes(layout, puv.cameras(sc.cameras[:1]))
+        per_view = sb1 + 1.3 * ah1
+        local_n = len(range(rank, n_views, world))
+        chunks = max(1, int(np.ceil(local_n * per_view / (0.5 * free))))
+        vpc = int(np.ceil(local_n / chunks))
+
+    frames = None
+    if cfg == 4:
+        n_frames = args.frames or sc.meta["frames"]
+        labels = torch.from_numpy(sc.levels[0].labels).to(dev)
+        stepper = FrameStep(layout, sc.cameras, n_frames, rank, world, dev, dynamic=labels, views_per_call=vpc)
+        pos = [torch.from_numpy(frame_positions(sc, f)).to(dev) for f in range(n_frames)]
+        frames = [[pos[f][0], pos[f][1], pos[f][2]] + [atlas[d] for d in range(3, D)] for f in range(n_frames)]
+        idx = stepper.local_targets_index()
+        tg_host = torch.empty((len(idx), 3, H, W), dtype=torch.float32).pin_memory()
+        for i, (f, v) in enumerate(idx):
+            tg_host[i].copy_(torch.from_numpy(sc.target(v, frame=f)))
+        targets = tg_host.to(dev)
+        grad = torch.zeros((n_frames, D, layout.atlas_h, layout.atlas_w), dtype=torch.float32, device=dev)
+        mask = labels
+        renders_per_step = n_frames * n_views
+        local_renders = len(idx)
+
+        def step(check=False):
+            return stepper.step(frames, occ, targets, grad, mask=mask, check_overflow=check)
+    else:
+        stepper = ShardedStep(layout, sc.cameras, rank, world, dev, views_per_call=vpc)
+        tg_host = torch.from_numpy(np.stack([sc.target(v) for v in stepper.views])).pin_memory()
+        targets = tg_host.to(dev)
+        grad = torch.zeros_like(atlas)
+        mask = None
+        renders_per_step = n_views
+        local_renders = len(stepper.views)
+
+        def step(check=False):
+            return stepper.step(atlas, occ, targets, grad, check_overflow=check)
     torch.cuda.synchronize()
 
-    # ---- warm-up (first step checks the key arena and grows it if needed) ----
+    # ---- warm-up (the first step checks the key arena and grows it if needed) ----
     for w in range(max(args.warmup, 1)):
-        grad.zero_()
-        stepper.step(atlas, occ, targets, grad, check_overflow=(w == 0))
+        step(check=(w == 0))
     torch.cuda.synchronize()
 
-    # ---- timed region: inputs resident in HBM ----
+    # ---- timed region: inputs resident in HBM (larger than L2: no flush needed) ----
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = puv.kernel_launches()
@@ -239,8 +340,7 @@ def main():
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            grad.zero_()
-            loss = stepper.step(atlas, occ, targets, grad)
+            loss = step()
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -254,19 +354,64 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     overflow = stepper.overflowed()
-    value = n_views / (ms_max / 1000.0)
+    value = renders_per_step / (ms_max / 1000.0)
+    loss_value = float(loss.item())
 
-    # ---- e2e: the same step through the public API with HOST inputs (pinned), H2D + D2H inside ----
+    # ---- serialised per-stage times: one extra (untimed) step with binning on the main stream ----
+    serial = None
+    if not args.no_serial:
+        puv.profile_serial(True)
+        puv.profile_enable(True)
+        step()
+        torch.cuda.synchronize()
+        puv.profile_enable(False)
+        puv.profile_serial(False)
+        sp = puv.profile_read(reset=True)
+        serial = {k: round(v / local_renders, 4) for k, v in sp["ms"].items() if v > 0}
+
+    # ---- e2e: the same step through the C ABI with HOST buffers (puv_train_step_host): inputs
+    # copied in from pinned memory and the step's result (gradient planes + loss) copied back ----
     e2e = None
     if not args.no_e2e:
-        atlas_host = atlas.cpu().pin_memory()
+        grad_host = torch.empty(tuple(grad.shape), dtype=torch.float32).pin_memory()
         loss_host = torch.zeros(1, dtype=torch.float64).pin_memory()
-        a_dev = torch.empty_like(atlas)
-        t_dev = torch.empty_like(targets)
+        if cfg == 4:
+            pos_host = [p.cpu().pin_memory() for p in pos]
+            shared_host = atlas[3:].cpu().pin_memory()
+            a_dev = torch.empty_like(atlas)
+            p_dev = [torch.empty_like(p) for p in pos]
+            fr_dev = [[p_dev[f][0], p_dev[f][1], p_dev[f][2]] + [a_dev[d] for d in range(3, D)]
+                      for f in range(len(pos))]
+            t_dev = torch.empty_like(targets)
 
-        def e2e_step():
-            grad.zero_()
-            stepper.step_host(atlas_host, occ, tg_host, grad, a_dev, t_dev, loss_host)
+            def e2e_step():
+                off = 0
+                for f in range(len(pos)):
+                    vs = stepper.frames.get(f, [])
+                    if not vs:
+                        grad[f].zero_()
+                        continue
+                    up = [(pos_host[f], p_dev[f])] + ([(shared_host, a_dev[3:])] if off == 0 else [])
+                    puv.train_step_host(layout, fr_dev[f], occ, stepper.cams[f], tg_host[off:off + len(vs)],
+                                        t_dev[off:off + len(vs)], grad[f], stepper.st, uploads=up,
+                                        downloads=[(grad[f], grad_host[f])] if world == 1 else [], mask=mask)
+                    stepper.losses[f:f + 1].copy_(stepper.st.loss)
+                    off += len(vs)
+                torch.sum(stepper.losses, dim=0, keepdim=True, out=stepper.loss)
+                if world > 1:
+                    dist.all_reduce(grad)
+                    dist.all_reduce(stepper.loss)
+                    grad_host.copy_(grad, non_blocking=True)
+                loss_host.copy_(stepper.loss, non_blocking=True)
+            h2d = sum(p.nbytes for p in pos_host) + shared_host.nbytes + tg_host.nbytes
+        else:
+            atlas_host = atlas.cpu().pin_memory()
+            a_dev = torch.empty_like(atlas)
+            t_dev = torch.empty_like(targets)
+
+            def e2e_step():
+                stepper.step_host(atlas_host, occ, tg_host, grad, a_dev, t_dev, grad_host, loss_host)
+            h2d = atlas_host.nbytes + tg_host.nbytes
 
         e2e_step()
         torch.cuda.synchronize()
@@ -281,84 +426,77 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_views / (float(te.item()) / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": int(atlas_host.numel() * 4 + tg_host.numel() * 4),
-               "d2h_bytes_per_step": 8}
+        e2e = {"value": renders_per_step / (float(te.item()) / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(grad_host.nbytes + loss_host.nbytes),
+               "api": "puv_train_step_host (C ABI, host buffers)"}
 
-    # ---- per-view counts (deterministic; read after timing) ----
+    # ---- per-view counts of the last render call on the state (deterministic; read after timing) ----
+    st = stepper.st
+    if cfg == 4:
+        last_views = stepper.frames[max(stepper.frames)]
+    else:
+        last_views = stepper.views
+    k0 = (len(last_views) - 1) // st.views_per_call * st.views_per_call
+    chunk_cams = puv.cameras([sc.cameras[v] for v in last_views[k0:]])
     counts = []
-    for i in range(len(mine)):
-        d = puv.debug_view(layout, stepper.cams, stepper.R.state, stepper.R.arena, i)
+    for i in range(len(chunk_cams)):
+        d = puv.debug_view(layout, chunk_cams, st.state, st.arena, i)
         counts.append({"n_vis": d.n_visible, "K": d.n_keys, "examined": d.n_examined, "composited": d.n_composited})
-    HW = sc.cameras[0].width * sc.cameras[0].height
-    c_tot = {k: sum(c[k] for c in counts) for k in ("n_vis", "K", "examined", "composited")}
+    c_tot = {k2: sum(c[k2] for c in counts) / len(counts) for k2 in ("n_vis", "K", "examined", "composited")}
 
-    # ---- roofline of the dominant stage ----
+    # ---- roofline of the dominant compositing kernel (SURVEY §8(d) basis) ----
     peaks = load_peaks()
-    sm_mhz = peaks["sm_max_mhz"]
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     stage_ms = {s: prof["ms"][s] / args.steps for s in prof["ms"]}
-    # depth_sort and bin run on the library's binning streams, overlapped with the compositing of
-    # earlier views: their event intervals include time-sharing, so they are not candidates for the
-    # dominant kernel (the ncu launch list in profiles/ gives their serialised share).
-    overlapped = ("depth_sort", "bin")
-    dom = max((s for s in stage_ms if s not in overlapped), key=lambda s: stage_ms[s])
-    per_view = {"N": atlas.shape[1] * atlas.shape[2], "views": len(mine), "HW": HW, "ntiles": 0,
-                "n_vis": c_tot["n_vis"] / len(mine), "K": c_tot["K"] / len(mine),
-                "examined": c_tot["examined"] / len(mine), "composited": c_tot["composited"] / len(mine)}
-    gx = (sc.cameras[0].width + 15) // 16
-    gy = (sc.cameras[0].height + 15) // 16
-    per_view["ntiles"] = gx * gy
-    calls = max(prof["calls"][dom] / args.steps, 1)
-    units = len(mine) if dom not in ("loss",) else 1
-    kind, work = stage_work(dom, per_view, layout.planes)
-    avg_launch_s = stage_ms[dom] / 1000.0 / calls
-    work_per_launch = work * units / calls
-    if kind == "hbm":
-        achieved = work_per_launch / avg_launch_s / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                "peak_source": peaks["source"]}
-    else:
-        lanes = 128 if kind == "alu_fp32" else 64
-        peak = nsm * lanes * sm_mhz * 1e6 / 1e12
-        achieved = work_per_launch / avg_launch_s / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak,
-                "unit": "T lane-ops/s (" + ("fp32" if kind == "alu_fp32" else "fp64") + ")",
-                "frac": achieved / peak, "traffic": None,
-                "peak_source": f"derived: {nsm} SMs x {lanes} {kind[4:]} lanes x {sm_mhz:.0f} MHz (DESIGN.md §6)"}
-    roof["kernel"] = dom
-    roof["work"] = {"raster_fwd": "18 fp64 lane-ops per composited pair + fp32 contract work at half weight "
-                                  "(8 per examined, 19 per composited pair)",
-                    "raster_bwd": "32 fp64 lane-ops per composited pair"}.get(dom, "algorithmic bytes, DESIGN.md §6")
-    roof["avg_launch_ms"] = avg_launch_s * 1000.0
+    gx, gy = (W + 15) // 16, (H + 15) // 16
+    per_view = {"N": N, "views": max(st.views_per_call, 1), "HW": W * H, "ntiles": gx * gy, **c_tot}
+    rf = {}
+    for s_ in ("raster_fwd", "raster_bwd"):
+        rf[s_] = roofline(s_, per_view, D, local_renders, stage_ms[s_], prof["calls"][s_] / args.steps, peaks, nsm)
+    dom = max(rf, key=lambda k2: stage_ms[k2])
+    roof = dict(rf[dom])
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp) and args.config == 3:
+    if os.path.exists(tp) and cfg == 3:
         tj = json.load(open(tp))
         if dom in tj.get("bytes_per_launch", {}):
-            # ncu capture of the same kernel on C3, scaled to this run's views per launch
-            roof["traffic"] = tj["bytes_per_launch"][dom] / tj["views_per_launch"][dom] * (units / calls)
-            roof["traffic_unit"] = "bytes/launch (ncu dram read+write)"
+            vpl = local_renders / max(prof["calls"][dom] / args.steps, 1)
+            roof["traffic"] = tj["bytes_per_launch"][dom] / tj["views_per_launch"][dom] * vpl
+            roof["traffic_unit"] = "bytes/launch (ncu dram read+write, profiles/traffic.json)"
+    other = "raster_bwd" if dom == "raster_fwd" else "raster_fwd"
+    roof["other_raster_kernel"] = {k2: rf[other][k2] for k2 in ("kernel", "achieved", "frac", "avg_launch_ms")}
+    hbm_stages = {}
+    for s_ in ("project", "project_bwd", "loss"):
+        if stage_ms.get(s_, 0) > 0:
+            r = roofline(s_, per_view, D, local_renders if s_ != "loss" else 1, stage_ms[s_],
+                         prof["calls"][s_] / args.steps, peaks, nsm)
+            hbm_stages[s_] = {"achieved_gbs": round(r["achieved"], 1), "frac": round(r["frac"], 3)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        vps, dt, cores = oracle_views_per_s(sc, list(range(args.cpu_sample_views)))
-        cpu = {"value": vps, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{args.cpu_sample_views} view(s) of {n_views}, full resolution fwd+bwd ({dt:.1f} s)"}
+        csc = sc if cfg != 4 else make_scene(3)
+        nv = args.cpu_sample_views
+        vps, dt, used = oracle_views_per_s(csc, list(range(nv)), threads=0)
+        vps1, dt1, _ = oracle_views_per_s(csc, [0], threads=1)
+        cpu = {"value": vps, "unit": UNIT, "cores": used, "kind": "oracle",
+               "sample": f"{nv} view(s) of {len(csc.cameras)} ({'C3 views for the C4 frames' if cfg == 4 else 'this config'}), "
+                         f"full resolution fwd+bwd, OpenMP over pixel rows ({dt:.1f} s)",
+               "single_thread": {"value": vps1, "unit": UNIT, "sample": f"1 view ({dt1:.1f} s)"}, **host_cpu()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32 decisions+forward / f64 backward values", "data": "synthetic",
-                "config": {"workload": WORKLOADS.get(args.config, str(args.config)), "views_per_step": n_views,
-                           "views_per_gpu": len(mine), "parallelism": f"view-sharded dp{world}",
-                           "l2": "inputs larger than L2 (atlas 247.5 MB, per-step state > 10 GB)"},
+                "vs_baseline": None, "dtype": "f32 decisions (bit-exact contract), f64 composite values",
+                "data": "synthetic",
+                "config": {"workload": WORKLOADS.get(cfg, str(cfg)), "view_renders_per_step": renders_per_step,
+                           "view_renders_per_gpu": local_renders, "views_per_call": st.views_per_call,
+                           "parallelism": f"view-sharded dp{world}",
+                           "l2": "inputs larger than L2 (atlas >= 247.5 MB, per-call state > 3 GB)"},
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
-                "cpu_baseline": cpu,
-                "stage_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
-                "overlapped_stages": list(overlapped),
-                "counts_per_view": {k: v / len(mine) for k, v in c_tot.items()},
-                "overflow": overflow, "loss": float(loss.item())}
+                "hbm_stages": hbm_stages, "cpu_baseline": cpu,
+                "stage_ms_per_step": {k2: round(v, 4) for k2, v in stage_ms.items() if v > 0},
+                "overlapped_stages": ["depth_sort", "bin"],
+                "stage_ms_per_view_serialised": serial,
+                "counts_per_view": c_tot, "overflow": overflow, "loss": loss_value}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -256,11 +256,67 @@ puv_status puv_render_l2_step(const puv_layout* layout, const float* const* atla
                               void* state, size_t state_bytes, void* arena, size_t arena_bytes,
                               float* const* atlas_grad, void* targets_ready, void* stream);
 
+/* Device buffers of a training step (puv_train_step / puv_train_step_host).  images and
+ * dL_dimages hold views_per_call views (n*3*H*W floats); loss: double, OVERWRITTEN with
+ * L = 1/2 sum over all views (R11); overflow (uint32) / arena_need (uint64): OVERWRITTEN with
+ * "some view chunk overflowed the key arena" and the largest arena bytes a chunk needed (the
+ * step's result is then incomplete: grow the arena to arena_need and re-run the step);
+ * state / arena as for puv_render_views with n_views = views_per_call. */
+typedef struct {
+  float* images;
+  float* dL_dimages;
+  double* loss;
+  uint32_t* overflow;
+  uint64_t* arena_need;
+  void* state;
+  size_t state_bytes;
+  void* arena;
+  size_t arena_bytes;
+} puv_step_buffers;
+
+/* One training step of the L2 harness over n_views views (rows a1-a9), in chunks of
+ * views_per_call views (<= 0: all in one chunk; the state is sized for one chunk, so a large
+ * rig fits HBM): per chunk puv_render_views, the L2 loss gradient against `targets` (device,
+ * n_views*3*H*W floats), the composite and projection backward.  atlas_grad (host table of D
+ * device planes) is OVERWRITTEN with dL/d(texel planes) summed over all views, x D_i when
+ * dynamic_mask is given.  Results equal the separate calls. */
+puv_status puv_train_step(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                          int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, const float* targets,
+                          const uint8_t* dynamic_mask, int32_t views_per_call, const puv_step_buffers* buffers,
+                          float* const* atlas_grad, void* stream);
+
+/* One host<->device copy: src / dst are a HOST and a DEVICE pointer (direction given by the call). */
+typedef struct {
+  const void* src;
+  void* dst;
+  size_t bytes;
+} puv_copy;
+
+/* puv_train_step from HOST inputs, end to end: enqueues on `stream` the `uploads`
+ * (host -> device, e.g. the atlas planes), copies targets_host (host, n_views*3*H*W floats) into
+ * `targets` (device) on an internal copy stream that overlaps the render (the first loss waits
+ * for it), runs the step, then the `downloads` (device -> host, e.g. the gradient planes and the
+ * loss).  Asynchronous like every call: synchronise `stream` before reading the downloads.
+ * Pinned host memory makes the copies asynchronous (pageable memory works, synchronously). */
+puv_status puv_train_step_host(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                               int32_t n_views, const puv_camera* cams, const puv_render_opts* opts,
+                               const puv_copy* uploads, int32_t n_uploads, const float* targets_host, float* targets,
+                               const uint8_t* dynamic_mask, int32_t views_per_call, const puv_step_buffers* buffers,
+                               float* const* atlas_grad, const puv_copy* downloads, int32_t n_downloads,
+                               void* stream);
+
 /* The one host synchronisation per step: waits for `stream`, then reports
  * whether any view of the last render overflowed the arena and the arena
  * bytes the call needs.  Host outputs. */
 puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, int32_t* overflowed,
                               uint64_t* needed_arena_bytes);
+
+/* The asynchronous form of puv_check_overflow for callers that chain several render calls
+ * (e.g. view chunks of one step) without a host sync: enqueues on `stream`
+ *   *flag |= (the last render call on `state` overflowed);
+ *   *needed_arena_bytes = max(*needed_arena_bytes, the arena bytes that call needed).
+ * flag, needed_arena_bytes: DEVICE pointers (uint32, uint64), caller-initialised. */
+puv_status puv_overflow_accumulate(const void* state, uint32_t* flag, uint64_t* needed_arena_bytes, void* stream);
 
 /* Per-view debug/parity view of the state (synchronises `stream`).  Host out.
  * Device pointers inside point into state/arena and stay valid until the next call. */
@@ -311,6 +367,10 @@ typedef struct {
   uint64_t calls[PUV_NUM_STAGES];
   uint64_t kernel_launches;
 } puv_profile;
+/* Measurement aid: with on != 0, later render calls run the depth sort and binning of each view
+ * on the caller's stream instead of the internal binning streams, so every stage runs alone and
+ * its per-stage event time (puv_profile_read) is its serialised cost.  Results are identical. */
+puv_status puv_profile_serial(int32_t on);
 puv_status puv_profile_enable(int32_t on);
 puv_status puv_profile_read(puv_profile* out, int32_t reset);
 

@@ -159,8 +159,16 @@ float orc_log_c(float y)
     return fmaf(fe, LN2_HI, fmaf(fe, LN2_LO, s * P));
 }
 
-void orc_exp_c_array(const float* x, float* y, int64_t n) { for (int64_t i = 0; i < n; ++i) y[i] = orc_exp_c(x[i]); }
-void orc_log_c_array(const float* x, float* y, int64_t n) { for (int64_t i = 0; i < n; ++i) y[i] = orc_log_c(x[i]); }
+void orc_exp_c_array(const float* x, float* y, int64_t n)
+{
+    #pragma omp parallel for schedule(static, 65536)
+    for (int64_t i = 0; i < n; ++i) y[i] = orc_exp_c(x[i]);
+}
+void orc_log_c_array(const float* x, float* y, int64_t n)
+{
+    #pragma omp parallel for schedule(static, 65536)
+    for (int64_t i = 0; i < n; ++i) y[i] = orc_log_c(x[i]);
+}
 
 /* ------------------------------------------------------------------------- */
 /* spherical harmonics (real basis, 3DGS sign convention; R3)       */

@@ -29,6 +29,7 @@ void count_launches(int n) { g_launches += (uint64_t)n; }
 struct ProfEvent { int stage; cudaEvent_t a, b; uint64_t launches; };
 static std::mutex g_prof_mu;
 static std::atomic<bool> g_prof_on{false};
+static std::atomic<bool> g_serial{false};   // puv_profile_serial: binning on the caller's stream
 static std::vector<ProfEvent> g_prof_events;
 static std::vector<cudaEvent_t> g_event_pool;
 
@@ -77,6 +78,7 @@ struct StreamSet {
   std::mutex mu;
   cudaStream_t s[kBinStreams] = {};
   cudaStream_t s2 = nullptr;     // per-view loss + composite backward of the fused L2 step
+  cudaStream_t cp = nullptr;     // host->device target uploads of puv_train_step_host
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> ev, fev;
   static cudaEvent_t pooled(std::vector<cudaEvent_t>& pool, int v) {
@@ -104,6 +106,7 @@ static StreamSet& stream_set(int /*n*/) {
     cudaEventCreateWithFlags(&ss->fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ss->join, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ss->s2, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ss->cp, cudaStreamNonBlocking);
     sets[dev] = ss;
   }
   return *sets[dev];
@@ -481,9 +484,10 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
   }
   // Views are composited in groups of kFwdGroup consecutive views per launch (grid.y), each
   // group once all its views are binned.
+  const bool serial = g_serial;
   for (int v = 0; v < n_views; ++v) {
     const int i = v % p.nscratch;
-    cudaStream_t bs = ss.s[i];
+    cudaStream_t bs = serial ? s : ss.s[i];
     void* scratch = (char*)state + p.scratch0 + (size_t)i * p.scratch_stride;
     { StageScope sc(PUV_STAGE_DEPTH_SORT, bs); launch_depth_sort(p, c.views, scratch, v, bs); }
     { StageScope sc(PUV_STAGE_BIN, bs); launch_bin(p, c.views, scratch, (uint32_t*)arena, v, bs); }
@@ -697,6 +701,106 @@ puv_status puv_render_l2_step(const puv_layout* layout, const float* const* atla
   return cuda_check("puv_render_l2_step");
 }
 
+// One training step in chunks of views (rows a1-a9): per chunk render, L2 loss gradient (the
+// loss accumulates over chunks), composite backward and projection backward into atlas_grad.
+static puv_status train_step_enqueue(const puv_layout* layout, const float* const* atlas_planes,
+                                     const uint8_t* atlas_occ, int32_t n_views, const puv_camera* cams,
+                                     const puv_render_opts* opts, const float* targets, const uint8_t* dynamic_mask,
+                                     int32_t views_per_call, const puv_step_buffers* b, float* const* atlas_grad,
+                                     cudaEvent_t targets_ready, cudaStream_t s) {
+  if (!b) return fail(PUV_E_INVALID_ARGUMENT, "buffers is NULL");
+  if (!targets || !b->images || !b->dL_dimages || !b->loss || !b->overflow || !b->arena_need)
+    return fail(PUV_E_INVALID_ARGUMENT, "NULL targets / images / dL_dimages / loss / overflow / arena_need");
+  if (!b->arena && b->arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "arena is NULL");
+  const int chunk = (views_per_call <= 0 || views_per_call > n_views) ? n_views : views_per_call;
+  Common c;
+  puv_status st = prepare(layout, atlas_planes, chunk, cams, opts, b->state, b->state_bytes, c);
+  if (st) return st;
+  st = check_cameras(n_views, cams, c.W, c.H);   // every camera, not only the first chunk's
+  if (st) return st;
+  GradTab G;
+  if ((st = grad_table(layout, atlas_grad, G))) return st;
+  const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
+  const size_t NA = (size_t)layout->atlas_w * layout->atlas_h, HW3 = (size_t)3 * c.W * c.H;
+  for (int d = 0; d < layout->planes; ++d)
+    if (G.p[d]) cudaMemsetAsync(G.p[d], 0, NA * sizeof(float), s);   // OVERWRITTEN: zero, then accumulate
+  cudaMemsetAsync(b->loss, 0, sizeof(double), s);
+  cudaMemsetAsync(b->overflow, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(b->arena_need, 0, sizeof(uint64_t), s);
+  for (int v0 = 0; v0 < n_views; v0 += chunk) {
+    const int n = n_views - v0 < chunk ? n_views - v0 : chunk;
+    Common cc = c;
+    cc.plan = make_plan(*layout, n, c.W, c.H);   // offsets of an n-view call (fits: n <= chunk)
+    cc.views = views_of(cc.plan, b->state);
+    render_pipeline(cc, atlas_occ, n, cams + v0, bg, b->images, b->state, b->arena, b->arena_bytes, s, nullptr);
+    launch_overflow_acc(b->state, b->overflow, b->arena_need, s);
+    if (targets_ready && v0 == 0) cudaStreamWaitEvent(s, targets_ready, 0);
+    { StageScope sc(PUV_STAGE_LOSS, s);
+      launch_l2_loss((int64_t)(n * HW3), b->images, targets + (size_t)v0 * HW3, b->dL_dimages, b->loss, s, true); }
+    cudaMemsetAsync(cc.views.grad2d, 0, (size_t)72 * n * cc.plan.N, s);
+    { StageScope sc(PUV_STAGE_RASTER_BWD, s);
+      launch_raster_bwd(cc.plan, cc.views, (const uint32_t*)b->arena, b->dL_dimages, 0, n, s); }
+    project_backward(cc, atlas_occ, n, cams + v0, dynamic_mask, G, s);
+  }
+  return PUV_OK;
+}
+
+puv_status puv_train_step(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                          int32_t n_views, const puv_camera* cams, const puv_render_opts* opts, const float* targets,
+                          const uint8_t* dynamic_mask, int32_t views_per_call, const puv_step_buffers* buffers,
+                          float* const* atlas_grad, void* stream) {
+  const puv_status st = train_step_enqueue(layout, atlas_planes, atlas_occ, n_views, cams, opts, targets, dynamic_mask,
+                                           views_per_call, buffers, atlas_grad, nullptr, (cudaStream_t)stream);
+  if (st) return st;
+  return cuda_check("puv_train_step");
+}
+
+puv_status puv_train_step_host(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
+                               int32_t n_views, const puv_camera* cams, const puv_render_opts* opts,
+                               const puv_copy* uploads, int32_t n_uploads, const float* targets_host, float* targets,
+                               const uint8_t* dynamic_mask, int32_t views_per_call, const puv_step_buffers* buffers,
+                               float* const* atlas_grad, const puv_copy* downloads, int32_t n_downloads,
+                               void* stream) {
+  if (n_uploads < 0 || n_downloads < 0 || (n_uploads && !uploads) || (n_downloads && !downloads))
+    return fail(PUV_E_INVALID_ARGUMENT, "bad upload / download lists");
+  for (int i = 0; i < n_uploads; ++i)
+    if (uploads[i].bytes && (!uploads[i].src || !uploads[i].dst)) return fail(PUV_E_INVALID_ARGUMENT, "upload %d", i);
+  for (int i = 0; i < n_downloads; ++i)
+    if (downloads[i].bytes && (!downloads[i].src || !downloads[i].dst))
+      return fail(PUV_E_INVALID_ARGUMENT, "download %d", i);
+  if (!targets || !targets_host) return fail(PUV_E_INVALID_ARGUMENT, "NULL targets");
+  int W, H;
+  puv_status st = check_cameras(n_views, cams, W, H);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  StreamSet& ss = stream_set(1);
+  // this call's own events (recorded once, destroyed after use: resources are released when
+  // the recorded work completes), so concurrent calls never share them
+  cudaEvent_t fork = nullptr, done = nullptr;
+  cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  {
+    std::lock_guard<std::mutex> lock(ss.mu);   // the copy stream is shared per device
+    // targets on the copy stream (after earlier work on `s` released the buffer), overlapping the render
+    cudaEventRecord(fork, s);
+    cudaStreamWaitEvent(ss.cp, fork, 0);
+    cudaMemcpyAsync(targets, targets_host, (size_t)n_views * 3 * W * H * sizeof(float), cudaMemcpyHostToDevice,
+                    ss.cp);
+    cudaEventRecord(done, ss.cp);
+  }
+  for (int i = 0; i < n_uploads; ++i)
+    if (uploads[i].bytes) cudaMemcpyAsync(uploads[i].dst, uploads[i].src, uploads[i].bytes, cudaMemcpyHostToDevice, s);
+  st = train_step_enqueue(layout, atlas_planes, atlas_occ, n_views, cams, opts, targets, dynamic_mask, views_per_call,
+                          buffers, atlas_grad, done, s);
+  cudaEventDestroy(fork);
+  cudaEventDestroy(done);
+  if (st) return st;
+  for (int i = 0; i < n_downloads; ++i)
+    if (downloads[i].bytes)
+      cudaMemcpyAsync(downloads[i].dst, downloads[i].src, downloads[i].bytes, cudaMemcpyDeviceToHost, s);
+  return cuda_check("puv_train_step_host");
+}
+
 puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, int32_t* overflowed,
                               uint64_t* needed_arena_bytes) {
   if (!state || !overflowed || !needed_arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "NULL argument");
@@ -708,6 +812,12 @@ puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, 
   *overflowed = (int32_t)h.overflow_any;
   *needed_arena_bytes = 4 * h.arena_need;
   return PUV_OK;
+}
+
+puv_status puv_overflow_accumulate(const void* state, uint32_t* flag, uint64_t* needed_arena_bytes, void* stream) {
+  if (!state || !flag || !needed_arena_bytes) return fail(PUV_E_INVALID_ARGUMENT, "NULL argument");
+  launch_overflow_acc(state, flag, needed_arena_bytes, (cudaStream_t)stream);
+  return cuda_check("puv_overflow_accumulate");
 }
 
 puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, const void* state,
@@ -782,6 +892,11 @@ puv_status puv_label_dynamic(const puv_layout* layout, const float* const* atlas
     launch_label(p, P, atlas_occ, cam_dev(cams[c]), masks + (size_t)c * W * H, (uint32_t*)workspace, r_max, c == 0,
                  labels, s);
   return cuda_check("puv_label_dynamic");
+}
+
+puv_status puv_profile_serial(int32_t on) {
+  g_serial = on != 0;
+  return PUV_OK;
 }
 
 puv_status puv_profile_enable(int32_t on) {

@@ -156,5 +156,6 @@ void launch_quant_fit(const PlaneTab& P, int D, const uint8_t* occ, int64_t N, f
 void launch_quantize(const float* const* x, float* const* proxy, void* const* code, const int8_t* bits, int D,
                      const float* spec, const uint8_t* occ, int64_t N, cudaStream_t s);
 void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaStream_t s);
+void launch_overflow_acc(const void* state, uint32_t* flag, uint64_t* need, cudaStream_t s);
 
 }  // namespace puv

@@ -130,4 +130,16 @@ void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaSt
   count_launches(1);
 }
 
+// flag |= overflow of the last render call on this state; need = max(need, its arena bytes)
+__global__ void k_overflow_acc(const CallHdr* call, uint32_t* flag, uint64_t* need) {
+  *flag |= call->overflow_any;
+  const uint64_t b = 4 * call->arena_need;
+  if (b > *need) *need = b;
+}
+
+void launch_overflow_acc(const void* state, uint32_t* flag, uint64_t* need, cudaStream_t s) {
+  k_overflow_acc<<<1, 1, 0, s>>>(reinterpret_cast<const CallHdr*>(state), flag, need);   // CallHdr at offset 0
+  count_launches(1);
+}
+
 }  // namespace puv

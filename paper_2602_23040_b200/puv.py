@@ -64,6 +64,16 @@ class ViewDebug(C.Structure):
                 ("depth_order", C.c_void_p), ("n_examined", C.c_uint64), ("n_composited", C.c_uint64)]
 
 
+class StepBuffers(C.Structure):
+    _fields_ = [("images", C.c_void_p), ("dL_dimages", C.c_void_p), ("loss", C.c_void_p), ("overflow", C.c_void_p),
+                ("arena_need", C.c_void_p), ("state", C.c_void_p), ("state_bytes", C.c_size_t),
+                ("arena", C.c_void_p), ("arena_bytes", C.c_size_t)]
+
+
+class Copy(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("bytes", C.c_size_t)]
+
+
 NUM_STAGES = 11
 STAGES = ("project", "depth_sort", "bin", "raster_fwd", "loss", "raster_bwd", "project_bwd", "pack", "label",
           "objective", "quant")
@@ -94,6 +104,9 @@ def lib():
         L.puv_render_backward.argtypes = [P, P, P, S, P, P, P, P, P, C.c_size_t, P, C.c_size_t, P, P]
         L.puv_render_l2_step.argtypes = [P, P, P, S, P, P, P, P, P, P, P, P, C.c_size_t, P, C.c_size_t, P, P, P]
         L.puv_check_overflow.argtypes = [P, S, P, P, P]
+        L.puv_overflow_accumulate.argtypes = [P, P, P, P]
+        L.puv_train_step.argtypes = [P, P, P, S, P, P, P, P, S, P, P, P]
+        L.puv_train_step_host.argtypes = [P, P, P, S, P, P, P, S, P, P, P, S, P, P, P, S, P]
         L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
         L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
         L.puv_layout_paper.argtypes = [S, S, S, P]
@@ -117,6 +130,8 @@ def lib():
         L.puv_quantize.argtypes = [P, P, P, P, S, S, P, P, P]
         L.puv_quantize.restype = C.c_int32
         L.puv_profile_enable.argtypes = [S]
+        L.puv_profile_serial.argtypes = [S]
+        L.puv_profile_serial.restype = C.c_int32
         L.puv_profile_read.argtypes = [P, S]
         L.puv_profile_enable.restype = C.c_int32
         L.puv_profile_read.restype = C.c_int32
@@ -125,7 +140,8 @@ def lib():
         L.puv_version.restype = C.c_char_p
         for f in ("puv_layout_for_levels", "puv_pack_atlas", "puv_unpack_levels", "puv_query_sizes",
                   "puv_render_views", "puv_l2_loss_grad", "puv_render_backward", "puv_check_overflow",
-                  "puv_debug_view", "puv_debug_contract"):
+                  "puv_debug_view", "puv_debug_contract", "puv_overflow_accumulate", "puv_train_step",
+                  "puv_train_step_host"):
             getattr(L, f).restype = C.c_int32
         _LIB = L
     return _LIB
@@ -402,6 +418,71 @@ def label_dynamic(layout, atlas, occ, cams, masks, r_max=64, labels=None, worksp
     return labels
 
 
+def _copies(pairs):
+    """[(src_tensor, dst_tensor), ...] -> (array of puv_copy, n); bytes = src.numel() * element size."""
+    arr = (Copy * max(len(pairs), 1))()
+    for i, (a, b) in enumerate(pairs):
+        assert a.is_contiguous() and b.is_contiguous() and a.nbytes == b.nbytes, "copy: contiguous, equal sizes"
+        arr[i] = Copy(a.data_ptr(), b.data_ptr(), a.nbytes)
+    return arr, len(pairs)
+
+
+class StepState:
+    """Device buffers of puv_train_step for chunks of `views_per_call` views (images, dL/dImage,
+    loss, overflow flags, state, key arena); the arena grows on overflow (TrainStep.run)."""
+
+    def __init__(self, layout, cams_chunk, device, arena_bytes=None, bg=(0.0, 0.0, 0.0)):
+        self.opts = opts(bg)
+        sb, hint = query_sizes(layout, cams_chunk, self.opts)
+        W, H = cams_chunk[0].width, cams_chunk[0].height
+        n = len(cams_chunk)
+        self.device = torch.device(device)
+        self.state = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        self.arena = torch.empty(arena_bytes if arena_bytes else hint, dtype=torch.uint8, device=self.device)
+        self.images = torch.empty((n, 3, H, W), dtype=torch.float32, device=self.device)
+        self.dL = torch.empty_like(self.images)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.flags = torch.zeros(2, dtype=torch.int64, device=self.device)   # [overflow (u32 in low word), need]
+        self.views_per_call = n
+
+    def buffers(self) -> StepBuffers:
+        b = StepBuffers()
+        b.images, b.dL_dimages, b.loss = self.images.data_ptr(), self.dL.data_ptr(), self.loss.data_ptr()
+        b.overflow, b.arena_need = self.flags.data_ptr(), self.flags.data_ptr() + 8
+        b.state, b.state_bytes = self.state.data_ptr(), self.state.numel()
+        b.arena, b.arena_bytes = self.arena.data_ptr(), self.arena.numel()
+        return b
+
+    def overflow(self):
+        """(overflowed, arena bytes needed) of the last step (synchronises)."""
+        f = self.flags.cpu()
+        return bool(int(f[0]) & 0xFFFFFFFF), int(f[1])
+
+    def grow(self, need):
+        self.arena = torch.empty(int(need * 1.1) + 4096, dtype=torch.uint8, device=self.device)
+
+
+def train_step(layout, atlas, occ, cams, targets, grad, st: StepState, mask=None, stream=None):
+    """puv_train_step: grad (D planes) OVERWRITTEN with dL/dtexels over all `cams`; st.loss = L."""
+    _check_images("targets", targets, len(cams), cams)
+    _ok(lib().puv_train_step(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams, C.byref(st.opts),
+                             _ptr(targets), _ptr(mask), st.views_per_call, C.byref(st.buffers()), _planes(grad),
+                             _stream(stream)))
+
+
+def train_step_host(layout, atlas, occ, cams, targets_host, targets, grad, st: StepState, uploads=(), downloads=(),
+                    mask=None, stream=None):
+    """puv_train_step_host: `uploads` / `downloads` are [(host, device)] / [(device, host)] tensor
+    pairs copied before / after the step; targets_host -> targets overlaps the render."""
+    _check_images("targets", targets, len(cams), cams)
+    assert not targets_host.is_cuda and targets_host.is_contiguous() and targets_host.numel() == targets.numel()
+    up, nu = _copies(list(uploads))
+    down, nd = _copies(list(downloads))
+    _ok(lib().puv_train_step_host(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams, C.byref(st.opts), up,
+                                  nu, _ptr(targets_host), _ptr(targets), _ptr(mask), st.views_per_call,
+                                  C.byref(st.buffers()), _planes(grad), down, nd, _stream(stream)))
+
+
 def check_overflow(state, n_views, stream=None):
     ov, need = C.c_int32(), C.c_uint64()
     _ok(lib().puv_check_overflow(_ptr(state), n_views, _stream(stream), C.byref(ov), C.byref(need)))
@@ -413,6 +494,11 @@ def debug_view(layout, cams, state, arena, view, stream=None) -> ViewDebug:
     _ok(lib().puv_debug_view(C.byref(layout), len(cams), cams, _ptr(state), state.numel(), _ptr(arena), view,
                              _stream(stream), C.byref(out)))
     return out
+
+
+def profile_serial(on: bool = True):
+    """Run each view's depth sort + binning on the caller's stream (serialised stage times)."""
+    _ok(lib().puv_profile_serial(1 if on else 0))
 
 
 def profile_enable(on: bool = True):

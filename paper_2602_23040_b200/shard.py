@@ -1,12 +1,21 @@
-"""View sharding over torch.distributed (row a10 of DESIGN.md §1).
+"""View sharding over torch.distributed (row a10 of DESIGN.md §1, SURVEY §8(e)).
 
 Cameras shard naturally across GPUs (BJ.north_star): rank r renders views
 v = r, r + n, r + 2n, ... (round-robin mixes the two camera rings of C3 so the
-per-rank key counts balance), accumulates its local atlas gradient with
-`render_backward` (+=), and the gradient planes are summed with ONE
-all-reduce over NCCL (NVLink 5 / NVSwitch).  The atlas is replicated.  The
-loss is summed the same way.  Everything here is orchestration: the render
-runs in libpuv's kernels.
+per-rank key counts balance), forms its local atlas gradient with one
+`puv_train_step` (render, L2 loss gradient, backward; in chunks of
+`views_per_call` views so a large rig fits HBM), and the gradient planes are
+summed with ONE all-reduce over NCCL (NVLink 5 / NVSwitch).  The atlas is
+replicated.  The loss is summed the same way.
+
+`FrameStep` is the temporal workload C4 (BJ.configs[3]): the (frame, view)
+pairs of a frame sequence are dealt round-robin over the ranks, each frame has
+its own atlas (plane table: per-frame position planes + shared constant
+planes) and its own gradient, and the frames' gradients are exchanged in one
+all-reduce restricted to the dynamic texels (static texels are frozen,
+PAPER.md:410-414, so their gradient is exactly zero on every rank).
+
+Everything here is orchestration: the render runs in libpuv's kernels.
 """
 from __future__ import annotations
 
@@ -20,6 +29,11 @@ def local_views(n_views: int, rank: int, world: int) -> list[int]:
     return [v for v in range(n_views) if v % world == rank]
 
 
+def local_pairs(n_frames: int, n_views: int, rank: int, world: int) -> list[tuple[int, int]]:
+    """C4: (frame, view) pairs p = frame * n_views + view with p mod world == rank."""
+    return [(p // n_views, p % n_views) for p in range(n_frames * n_views) if p % world == rank]
+
+
 def reduce_gradients(grad: torch.Tensor, loss: torch.Tensor, world: int, group=None) -> None:
     """The one exchange of the path (row a10): sum the atlas gradient planes and the loss over ranks."""
     if world > 1:
@@ -28,67 +42,136 @@ def reduce_gradients(grad: torch.Tensor, loss: torch.Tensor, world: int, group=N
 
 
 class ShardedStep:
-    """One fwd + loss + bwd step over this rank's views, then the gradient all-reduce."""
+    """One fwd + loss + bwd step over this rank's views (puv_train_step), then the all-reduce."""
 
     def __init__(self, layout, cameras, rank=0, world=1, device="cuda", bg=(0.0, 0.0, 0.0), arena_bytes=None,
-                 group=None):
+                 group=None, views_per_call=None):
+        self.layout = layout
         self.rank, self.world, self.group = rank, world, group
         self.views = local_views(len(cameras), rank, world)
         if not self.views:
             raise ValueError(f"rank {rank} of {world} has no views (n_views={len(cameras)})")
         self.device = torch.device(device)
         self.cams = puv.cameras([cameras[v] for v in self.views])
-        self.R = puv.Renderer(layout, self.cams, bg=bg, device=self.device, arena_bytes=arena_bytes)
-        self.images = torch.empty(self.R.image_shape, dtype=torch.float32, device=self.device)
-        self.dL = torch.empty_like(self.images)
-        self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+        vpc = min(views_per_call or len(self.views), len(self.views))
+        self.views_per_call = vpc
+        self.st = puv.StepState(layout, puv.cameras([cameras[v] for v in self.views[:vpc]]), self.device,
+                                arena_bytes=arena_bytes, bg=bg)
+
+    @property
+    def loss(self):
+        return self.st.loss
 
     def step(self, atlas, occ, targets, grad, mask=None, check_overflow=True):
-        """targets: (n_local, 3, H, W) fp32 on device; grad: (D, H_A, W_A) fp32, zeroed by the caller.
-        Returns the (device) loss, summed over ranks when world > 1.
+        """targets: (n_local, 3, H, W) fp32 on device; grad: (D, H_A, W_A) fp32, OVERWRITTEN with the
+        gradient summed over all ranks' views.  Returns the (device) loss, summed over ranks.
 
-        check_overflow (default on): after the forward, read the key-arena overflow flag (one host
-        sync) and, if a view did not fit, grow the arena and re-render before the loss and the
-        backward, so an overflowed view can never contribute a wrong gradient.  Callers that have
-        sized the arena already (the bench, after its first warm-up step) opt out explicitly and
-        check `overflowed()` after their timed region."""
-        # The separate calls, not the fused puv_render_l2_step: the fused pipeline measured the same
-        # step time on C3 (118.7 ms both, the GPU is already saturated by the compositing and the
-        # binning streams), and the separate calls keep each stage alone on its stream, so the
-        # per-stage CUDA-event times the bench reports are not shared with concurrent stages.
-        if check_overflow:   # sizes the key arena (grow and re-render)
-            self.R.forward(atlas, occ, images=self.images, check=True)
-        else:
-            puv.render_views(self.R.layout, atlas, occ, self.cams, self.R.opts, self.images, self.R.state,
-                             self.R.arena)
-        puv.l2_loss_grad(self.images, targets, self.dL, self.loss)
-        self.R.backward(atlas, occ, self.dL, grad=grad, mask=mask)
-        reduce_gradients(grad, self.loss, self.world, self.group)
-        return self.loss
+        check_overflow (default on): after the step, read the key-arena overflow flag (one host
+        sync) and, if a view chunk did not fit, grow the arena and re-run the step, so an
+        overflowed view can never contribute a wrong gradient.  Callers that have sized the arena
+        already (the bench, after its first warm-up step) opt out explicitly and check
+        `overflowed()` after their timed region."""
+        while True:
+            puv.train_step(self.layout, atlas, occ, self.cams, targets, grad, self.st, mask=mask)
+            if not check_overflow:
+                break
+            ov, need = self.st.overflow()
+            if not ov:
+                break
+            self.st.grow(need)
+        reduce_gradients(grad, self.st.loss, self.world, self.group)
+        return self.st.loss
 
-    def step_host(self, atlas_host, occ, targets_host, grad, atlas_dev, targets_dev, loss_host, mask=None):
-        """The same step from HOST inputs (the end-to-end call): the atlas is copied in first on the
-        current stream (K1 reads all of it), the targets on a side copy stream so that their
-        host->device transfer overlaps the render; the loss kernel waits for them.  The
-        (rank-summed) loss is read back into `loss_host`.  Host tensors must be pinned for the
-        copies to be asynchronous."""
-        cur = torch.cuda.current_stream(self.device)
-        if not hasattr(self, "_copy_stream"):
-            self._copy_stream = torch.cuda.Stream(device=self.device)
-            self._targets_ready = torch.cuda.Event()
-        self._copy_stream.wait_stream(cur)          # targets_dev is free once the previous step's loss ran
-        with torch.cuda.stream(self._copy_stream):
-            targets_dev.copy_(targets_host, non_blocking=True)
-            self._targets_ready.record(self._copy_stream)
-        atlas_dev.copy_(atlas_host, non_blocking=True)
-        puv.render_views(self.R.layout, atlas_dev, occ, self.cams, self.R.opts, self.images, self.R.state,
-                         self.R.arena)
-        cur.wait_event(self._targets_ready)
-        puv.l2_loss_grad(self.images, targets_dev, self.dL, self.loss)
-        self.R.backward(atlas_dev, occ, self.dL, grad=grad, mask=mask)
-        reduce_gradients(grad, self.loss, self.world, self.group)
-        loss_host.copy_(self.loss, non_blocking=True)
+    def step_host(self, atlas_host, occ, targets_host, grad, atlas_dev, targets_dev, grad_host, loss_host,
+                  mask=None):
+        """The same step from HOST inputs, end to end (puv_train_step_host): the atlas is uploaded
+        first (K1 reads all of it), the targets on the library's copy stream overlapping the
+        render, and the result -- the gradient planes and the loss -- is copied back into
+        `grad_host` / `loss_host`.  With world > 1 the download follows the all-reduce.  Host
+        tensors should be pinned (asynchronous copies).  Synchronise before reading the results."""
+        downloads = [(grad, grad_host), (self.st.loss, loss_host)] if self.world == 1 else []
+        puv.train_step_host(self.layout, atlas_dev, occ, self.cams, targets_host, targets_dev, grad, self.st,
+                            uploads=[(atlas_host, atlas_dev)], downloads=downloads, mask=mask)
+        if self.world > 1:
+            reduce_gradients(grad, self.st.loss, self.world, self.group)
+            grad_host.copy_(grad, non_blocking=True)
+            loss_host.copy_(self.st.loss, non_blocking=True)
         return loss_host
 
     def overflowed(self) -> bool:
-        return puv.check_overflow(self.R.state, len(self.views))[0]
+        """Whether any view chunk of the last step overflowed the key arena (synchronises)."""
+        return self.st.overflow()[0]
+
+
+class FrameStep:
+    """C4 (BJ.configs[3]): one step renders every (frame, view) pair of a frame sequence fwd + bwd.
+
+    Pairs are dealt round-robin over the ranks; per frame the local views run as one
+    puv_train_step (chunks of `views_per_call`) into that frame's gradient, with gradient
+    freezing by the dynamic labels.  Then ONE all-reduce sums the frames'
+    gradients over the dynamic texels only (the static ones are zero on every rank), and the
+    frames' losses are summed."""
+
+    def __init__(self, layout, cameras, n_frames, rank=0, world=1, device="cuda", dynamic=None, bg=(0.0, 0.0, 0.0),
+                 arena_bytes=None, group=None, views_per_call=None):
+        self.layout = layout
+        self.rank, self.world, self.group = rank, world, group
+        self.n_frames, self.n_views = n_frames, len(cameras)
+        self.device = torch.device(device)
+        self.pairs = local_pairs(n_frames, len(cameras), rank, world)
+        if not self.pairs:
+            raise ValueError(f"rank {rank} of {world} has no (frame, view) pairs")
+        self.frames = {}
+        for f, v in self.pairs:
+            self.frames.setdefault(f, []).append(v)
+        self.cams = {f: puv.cameras([cameras[v] for v in vs]) for f, vs in self.frames.items()}
+        vmax = max(len(vs) for vs in self.frames.values())
+        vpc = min(views_per_call or vmax, vmax)
+        self.views_per_call = vpc
+        self.st = puv.StepState(layout, puv.cameras([cameras[0]] * vpc), self.device, arena_bytes=arena_bytes, bg=bg)
+        self.losses = torch.zeros(n_frames, dtype=torch.float64, device=self.device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+        # dynamic texel ids (flattened atlas index) for the compacted exchange; None = all texels
+        self.dyn = None if dynamic is None else torch.nonzero(dynamic.reshape(-1)).reshape(-1).to(self.device)
+
+    def local_targets_index(self):
+        """[(frame, view)] in the order `step` expects the targets: frame-major, local views."""
+        return [(f, v) for f in sorted(self.frames) for v in self.frames[f]]
+
+    def step(self, frame_planes, occ, targets, grads, mask=None, check_overflow=True):
+        """frame_planes: per frame a plane table (D CUDA planes; constant planes may be shared);
+        targets: (n_local_pairs, 3, H, W) fp32 in `local_targets_index()` order; grads:
+        (n_frames, D, H_A, W_A) fp32, OVERWRITTEN with each frame's gradient summed over ranks;
+        mask: the dynamic labels D_i (H_A, W_A) uint8 (gradient freezing).  Returns the loss."""
+        off = 0
+        self.losses.zero_()
+        for f in range(self.n_frames):
+            vs = self.frames.get(f)
+            if not vs:
+                grads[f].zero_()   # no local view of this frame: it contributes nothing on this rank
+                continue
+            tg = targets[off:off + len(vs)]
+            off += len(vs)
+            while True:
+                puv.train_step(self.layout, frame_planes[f], occ, self.cams[f], tg, grads[f], self.st, mask=mask)
+                if not check_overflow:
+                    break
+                ov, need = self.st.overflow()
+                if not ov:
+                    break
+                self.st.grow(need)
+            self.losses[f:f + 1].copy_(self.st.loss)
+        torch.sum(self.losses, dim=0, keepdim=True, out=self.loss)
+        if self.world > 1:
+            if self.dyn is None:
+                dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=self.group)
+            else:   # the frozen (static) texels carry exact zeros: exchange the dynamic ones only
+                flat = grads.view(self.n_frames, grads.shape[1], -1)
+                buf = flat.index_select(2, self.dyn)
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+                flat.index_copy_(2, self.dyn, buf)
+            dist.all_reduce(self.loss, op=dist.ReduceOp.SUM, group=self.group)
+        return self.loss
+
+    def overflowed(self) -> bool:
+        return self.st.overflow()[0]

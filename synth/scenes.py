@@ -79,10 +79,12 @@ class Scene:
     def D(self) -> int:
         return n_planes(self.sh_degree)
 
-    def target(self, view: int) -> np.ndarray:
-        """Seeded U[0,1] target image (3, H, W) float32 for `view` (BJ.configs[0])."""
+    def target(self, view: int, frame: int | None = None) -> np.ndarray:
+        """Seeded U[0,1] target image (3, H, W) float32 for `view` (BJ.configs[0]); for a frame
+        sequence (C4) one image per (frame, view)."""
         cam = self.cameras[view]
-        rng = np.random.default_rng(np.random.SeedSequence([*SEED_ROOT, self.cfg, 1, view]))
+        seq = [*SEED_ROOT, self.cfg, 1, view] if frame is None else [*SEED_ROOT, self.cfg, 3, frame, view]
+        rng = np.random.default_rng(np.random.SeedSequence(seq))
         return rng.random((3, cam.height, cam.width), dtype=np.float32)
 
 

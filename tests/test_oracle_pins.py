@@ -80,6 +80,31 @@ def test_log_c_accuracy_and_specials():
 # SH basis (R3): orthonormal on the sphere (pins every constant and
 # polynomial; a wrong constant breaks normality, a wrong polynomial orthogonality)
 
+def test_sh_basis_signs_vs_scipy_legendre():
+    """Every basis function, sign included, against an independent construction (R3):
+    the real SH formed from scipy's complex Y_l^m (associated Legendre functions WITH the
+    Condon-Shortley phase (-1)^m) as  Y_{l,m} = sqrt2 Re Y_l^m (m > 0),  Y_l^0 (m = 0),
+    sqrt2 Im Y_l^|m| (m < 0), index k = l^2 + l + m.  This is the convention of the 3DGS
+    constants the paper's renderer inherits: at degree 1 it is sqrt(3/4pi) (-y, z, -x).
+    Orthonormality alone would accept any sign flip; this pin does not."""
+    from scipy.special import sph_harm_y
+    rng = np.random.default_rng(7)
+    d = rng.normal(size=(500, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    polar = np.arccos(np.clip(d[:, 2], -1, 1))
+    azim = np.arctan2(d[:, 1], d[:, 0])
+    ref = np.zeros((d.shape[0], 16))
+    for l in range(4):
+        for m in range(-l, l + 1):
+            c = sph_harm_y(l, abs(m), polar, azim)     # complex, Condon-Shortley phase included
+            ref[:, l * l + l + m] = (math.sqrt(2) * c.real if m > 0 else
+                                     (c.real if m == 0 else math.sqrt(2) * c.imag))
+    Y = orc.sh_basis(3, d)
+    assert np.abs(Y - ref).max() < 1e-12, np.abs(Y - ref).max(axis=0)
+    c1 = math.sqrt(3 / (4 * math.pi))
+    assert np.allclose(Y[:, 1:4], c1 * np.stack([-d[:, 1], d[:, 2], -d[:, 0]], 1), atol=1e-14)
+
+
 def test_sh_basis_orthonormal():
     nt, nph = 64, 48
     xg, wg = np.polynomial.legendre.leggauss(nph)             # exact in cos(phi) for deg <= 95

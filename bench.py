@@ -467,7 +467,7 @@ def main():
     hbm_stages = {}
     for s_ in ("project", "project_bwd", "loss"):
         if stage_ms.get(s_, 0) > 0:
-            r = roofline(s_, per_view, D, local_renders if s_ != "loss" else 1, stage_ms[s_],
+            r = roofline(s_, per_view, D, local_renders, stage_ms[s_],
                          prof["calls"][s_] / args.steps, peaks, nsm)
             hbm_stages[s_] = {"achieved_gbs": round(r["achieved"], 1), "frac": round(r["frac"], 3)}
 

@@ -41,6 +41,23 @@ def reduce_gradients(grad: torch.Tensor, loss: torch.Tensor, world: int, group=N
         dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
 
 
+def reduce_frame_gradients(grads: torch.Tensor, loss: torch.Tensor, world: int, dyn=None, group=None) -> None:
+    """C4's exchange: sum the per-frame gradients (n_frames, D, H_A, W_A) and the loss over ranks.
+    With `dyn` (flattened ids of the dynamic texels) only those texels are exchanged: gradient
+    freezing makes every static texel's gradient exactly zero on every rank, so
+    the compacted exchange is lossless and moves |dyn| / (H_A W_A) of the bytes (~25 % on C4)."""
+    if world <= 1:
+        return
+    if dyn is None:
+        dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group)
+    else:
+        flat = grads.view(grads.shape[0], grads.shape[1], -1)
+        buf = flat.index_select(2, dyn)
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        flat.index_copy_(2, dyn, buf)
+    dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
+
+
 class ShardedStep:
     """One fwd + loss + bwd step over this rank's views (puv_train_step), then the all-reduce."""
 
@@ -162,15 +179,7 @@ class FrameStep:
                 self.st.grow(need)
             self.losses[f:f + 1].copy_(self.st.loss)
         torch.sum(self.losses, dim=0, keepdim=True, out=self.loss)
-        if self.world > 1:
-            if self.dyn is None:
-                dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=self.group)
-            else:   # the frozen (static) texels carry exact zeros: exchange the dynamic ones only
-                flat = grads.view(self.n_frames, grads.shape[1], -1)
-                buf = flat.index_select(2, self.dyn)
-                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
-                flat.index_copy_(2, self.dyn, buf)
-            dist.all_reduce(self.loss, op=dist.ReduceOp.SUM, group=self.group)
+        reduce_frame_gradients(grads, self.loss, self.world, self.dyn, self.group)
         return self.loss
 
     def overflowed(self) -> bool:

@@ -88,3 +88,50 @@ def test_c5_one_view_4k():
     g_ref = orc.backward(planes, occ, 3, sc.cameras[v], dl)
     bad = grad_violations(grad, g_ref)
     assert not bad.any(), describe_violations(grad, g_ref, bad)
+
+
+def test_c4_frame_step_equals_per_frame_steps_and_oracle():
+    """FrameStep (the C4 bench path): (frame, view) pairs of frames {0, 29} x views {0, 27, 54} in one
+    step, each frame's gradient frozen by the dynamic labels.  Each frame's gradient equals a
+    separate puv_train_step of that frame (up to fp64 atomic order) and the oracle's on the same
+    dL/dImage; static texels are exactly zero; the loss is the sum of the frames'."""
+    from paper_2602_23040_b200.shard import FrameStep
+    sc = make_scene(4)
+    dev = torch.device("cuda")
+    lv = sc.levels[0]
+    layout = puv.layout_for_levels([(lv.rows, lv.cols)], 3)
+    base = torch.from_numpy(lv.planes).to(dev)
+    occ_t = torch.from_numpy(lv.occ).to(dev)
+    mask = lv.labels.astype(np.uint8)
+    mask_t = torch.from_numpy(mask).to(dev)
+    frames, views = [0, 29], [0, 27, 54]
+    cams_all = [sc.cameras[v] for v in views]
+    pos = [torch.from_numpy(frame_positions(sc, f)).to(dev) for f in frames]
+    tables = [[p[0], p[1], p[2]] + [base[d] for d in range(3, layout.planes)] for p in pos]
+    fs = FrameStep(layout, cams_all, len(frames), device=dev, dynamic=mask_t)
+    idx = fs.local_targets_index()
+    tg = torch.from_numpy(np.stack([sc.target(views[v], frame=frames[f]) for f, v in idx])).to(dev)
+    grads = torch.full((2, layout.planes, lv.rows, lv.cols), 3.0, device=dev)   # OVERWRITTEN
+    loss = fs.step(tables, occ_t, tg, grads, mask=mask_t).item()
+    G = grads.cpu().numpy().astype(np.float64)
+    assert np.all(G[:, :, mask == 0] == 0)
+    orc.set_threads(0)
+    L_sum = 0.0
+    for fi, f in enumerate(frames):
+        st = puv.StepState(layout, puv.cameras(cams_all), dev)
+        g1 = torch.empty_like(base)
+        puv.train_step(layout, tables[fi], occ_t, puv.cameras(cams_all), tg[3 * fi:3 * fi + 3], g1, st, mask=mask_t)
+        torch.cuda.synchronize()
+        L_sum += st.loss.item()
+        a = g1.cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(G[fi] - a) <= 1e-6 * np.abs(a) + 1e-30)
+        planes = lv.planes.copy()
+        planes[0:3] = frame_positions(sc, f)
+        val = planes.astype(np.float64)
+        dL = st.dL.cpu().numpy().astype(np.float64)
+        g_ref = np.zeros(planes.shape)
+        for vi, v in enumerate(views):
+            orc.backward(planes, lv.occ, 3, sc.cameras[v], dL[vi], mask=mask, val=val, grad=g_ref)
+        bad = grad_violations(a, g_ref)
+        assert not bad.any(), describe_violations(a, g_ref, bad)
+    assert abs(loss - L_sum) <= 1e-12 * L_sum

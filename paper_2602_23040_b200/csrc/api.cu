@@ -102,7 +102,13 @@ static StreamSet& stream_set(int /*n*/) {
   if ((int)sets.size() <= dev) sets.resize(dev + 1, nullptr);
   if (!sets[dev]) {
     StreamSet* ss = new StreamSet();
-    for (int i = 0; i < kBinStreams; ++i) cudaStreamCreateWithFlags(&ss->s[i], cudaStreamNonBlocking);
+    // The binning streams run at the device's highest stream priority: their kernels are small and
+    // latency bound, and the compositing of the previous view (a full-GPU grid on the caller's
+    // stream) must not starve them, or the next view's compositing waits for its tile lists.
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    for (int i = 0; i < kBinStreams; ++i)
+      cudaStreamCreateWithPriority(&ss->s[i], cudaStreamNonBlocking, kBinPriority ? prio_hi : prio_lo);
     cudaEventCreateWithFlags(&ss->fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ss->join, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ss->s2, cudaStreamNonBlocking);

@@ -16,6 +16,10 @@ constexpr int kNbMax = 1024;              // max key blocks of the stable tile p
 #define PUV_BIN_STREAMS 4
 #endif
 constexpr int kBinStreams = PUV_BIN_STREAMS;  // views binned concurrently (one scratch block each)
+#ifndef PUV_BIN_PRIORITY
+#define PUV_BIN_PRIORITY 1
+#endif
+constexpr int kBinPriority = PUV_BIN_PRIORITY;  // binning streams at the highest stream priority
 #ifndef PUV_DMASK
 #define PUV_DMASK 1
 #endif

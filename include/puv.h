@@ -207,7 +207,12 @@ puv_status puv_reg_loss_grad(const puv_layout* layout, const float* const* atlas
  * (16 and 8; each 1..16).  Unoccupied texels: code 0, proxy 0.  codes: NULL, or a
  * host table of D device pointers to uint8 planes (bits <= 8) / uint16 planes (bits > 8; the two
  * bytes are the hi/lo 8-bit planes of SPEC.md:313); proxy: NULL or a host table of D device fp32
- * planes.  Entries for rho mode's planes 1, 2 are ignored (may be NULL). */
+ * planes.  Entries for rho mode's planes 1, 2 are ignored (may be NULL).
+ * pos_bits = PUV_QUANT_FP16 (reading Q8, "we retain them in FP16"): the position
+ * planes are instead stored as IEEE binary16 (round to nearest even; the range is not used):
+ * code = the 16-bit pattern (uint16 plane; its two bytes are the 8-bit storage split of
+ * PAPER.md:1303), proxy = the half's value. */
+#define PUV_QUANT_FP16 256
 puv_status puv_quant_fit(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,
                          float* spec, void* stream);
 puv_status puv_quantize(const puv_layout* layout, const float* const* atlas_planes, const uint8_t* atlas_occ,

@@ -81,6 +81,11 @@ def lib():
         L.orc_dequant.argtypes = [C.c_uint32, C.c_float, C.c_float, C.c_int]
         L.orc_quant_fit.argtypes = [C.c_int, P, P, C.c_int64, P]
         L.orc_quantize_plane.argtypes = [P, P, C.c_int64, C.c_float, C.c_float, C.c_int, P, P]
+        L.orc_fp16_bits.restype = C.c_uint32
+        L.orc_fp16_bits.argtypes = [C.c_float]
+        L.orc_fp16_value.restype = C.c_float
+        L.orc_fp16_value.argtypes = [C.c_uint32]
+        L.orc_quantize_plane_fp16.argtypes = [P, P, C.c_int64, P, P]
         L.orc_pack.argtypes = [C.c_int, P, P, P, C.c_int, P, P, C.c_int32, C.c_int32, P, P]
         _LIB = L
     return _LIB
@@ -208,15 +213,32 @@ def quant_fit(planes, occ, skip=()):
     return spec
 
 
+FP16 = "fp16"   # bits value of a plane stored as IEEE binary16 (reading Q8)
+
+
+def fp16_bits(x):
+    """binary16 bit patterns (uint32) of fp32 values, round to nearest even (reading Q8)."""
+    x = np.ascontiguousarray(x, np.float32)
+    code = np.zeros(x.shape, np.uint32)
+    proxy = np.zeros(x.shape, np.float32)
+    lib().orc_quantize_plane_fp16(_ptr(x), None, x.size, _ptr(code), _ptr(proxy))
+    return code, proxy
+
+
 def quantize(planes, occ, spec, bits):
-    """Per plane d with bits[d] > 0: codes (uint32) and the fp32 proxy; planes with bits 0 are copied
-    through unchanged with code 0 (the unused planes 1, 2 of rho mode)."""
+    """Per plane d with bits[d] > 0: codes (uint32) and the fp32 proxy; bits[d] == FP16: the binary16
+    pattern and value; planes with bits 0 are copied through unchanged with code 0 (the unused
+    planes 1, 2 of rho mode)."""
     planes = np.ascontiguousarray(planes, np.float32)
     o = np.ascontiguousarray(occ, np.uint8) if occ is not None else None
     codes = np.zeros(planes.shape, np.uint32)
     proxy = planes.copy()
     for d in range(planes.shape[0]):
         if bits[d] == 0:
+            continue
+        if bits[d] == FP16:
+            lib().orc_quantize_plane_fp16(_ptr(planes[d]), None if o is None else _ptr(o), planes[d].size,
+                                          _ptr(codes[d]), _ptr(proxy[d]))
             continue
         lib().orc_quantize_plane(_ptr(planes[d]), None if o is None else _ptr(o), planes[d].size,
                                  float(spec[d, 0]), float(spec[d, 1]), int(bits[d]), _ptr(codes[d]), _ptr(proxy[d]))

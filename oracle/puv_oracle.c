@@ -1030,6 +1030,62 @@ float orc_dequant(uint32_t code, float mn, float mx, int bits)
     return mn + ((float)code / L) * (mx - mn);
 }
 
+/* Reading Q8: "we retain them [positions] in FP16" -- the position
+ * planes stored as IEEE 754 binary16.  fp32 -> binary16 with round-to-nearest-even, written out on
+ * the bit fields: sign; exponent rebiased 127 -> 15; normal halves keep 10 mantissa bits; values
+ * below 2^-14 become subnormal halves (mantissa shifted right with the implicit 1); overflow past
+ * the largest half (65504) -> infinity; NaN -> the quiet NaN 0x7e00.  Returns the 16-bit pattern. */
+uint32_t orc_fp16_bits(float x)
+{
+    const uint32_t b = bits_from_f(x);
+    const uint32_t sign = (b >> 16) & 0x8000u;
+    const int32_t e = (int32_t)((b >> 23) & 0xffu);
+    uint32_t m = b & 0x7fffffu;
+    if (e == 0xff) return sign | (m ? 0x7e00u : 0x7c00u);         /* inf / NaN */
+    int32_t he = e - 127 + 15;                                     /* half exponent field */
+    if (he >= 0x1f) return sign | 0x7c00u;                         /* too large: inf */
+    uint32_t mant;                                                 /* 1.m as a 24-bit integer (normal) */
+    int shift;                                                     /* bits dropped */
+    if (he <= 0) {                                                 /* subnormal half (or zero) */
+        if (e == 0) return sign;                                   /* fp32 zero / subnormal: |x| < 2^-126 */
+        mant = m | 0x800000u;
+        shift = 13 + 1 - he;
+        if (shift > 24) return sign;                               /* below half the smallest subnormal */
+        he = 0;
+    } else {
+        mant = m;
+        shift = 13;
+    }
+    uint32_t q = mant >> shift;
+    const uint32_t rem = mant & ((1u << shift) - 1u), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (q & 1u))) q += 1u;          /* round to nearest, ties to even */
+    /* a carry out of the mantissa bumps the exponent (also subnormal -> smallest normal, max -> inf) */
+    return sign | ((((uint32_t)he << 10) + q) & 0xffffu);
+}
+
+/* The binary16 value of a 16-bit pattern, as fp32 (exact). */
+float orc_fp16_value(uint32_t h)
+{
+    const uint32_t sign = (h & 0x8000u) << 16;
+    const uint32_t e = (h >> 10) & 0x1fu, m = h & 0x3ffu;
+    if (e == 0x1f) return f_from_bits(sign | 0x7f800000u | (m << 13));
+    if (e == 0) {                                                  /* subnormal: m * 2^-24 */
+        const float v = (float)m * 5.9604644775390625e-8f;
+        return sign ? -v : v;
+    }
+    return f_from_bits(sign | ((e - 15 + 127) << 23) | (m << 13));
+}
+
+/* Position plane stored as binary16: code = the 16-bit pattern, proxy = its value; unoccupied 0. */
+void orc_quantize_plane_fp16(const float* x, const uint8_t* occ, int64_t n, uint32_t* code, float* proxy)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        if (occ && !occ[i]) { code[i] = 0; proxy[i] = 0.0f; continue; }
+        code[i] = orc_fp16_bits(x[i]);
+        proxy[i] = orc_fp16_value(code[i]);
+    }
+}
+
 /* Per-plane min/max over occupied texels; no occupied texel -> (0, 0). */
 void orc_quant_fit(int D, const float* const* planes, const uint8_t* occ, int64_t n, float* spec /* D x 2 */)
 {

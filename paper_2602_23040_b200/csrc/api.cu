@@ -570,8 +570,8 @@ puv_status puv_quantize(const puv_layout* layout, const float* const* atlas_plan
   puv_status st = check_layout(layout);
   if (st) return st;
   if (!atlas_planes || !spec) return fail(PUV_E_INVALID_ARGUMENT, "NULL pointer");
-  if (pos_bits < 1 || pos_bits > 16 || attr_bits < 1 || attr_bits > 16)
-    return fail(PUV_E_INVALID_ARGUMENT, "bits (%d, %d) outside 1..16", pos_bits, attr_bits);
+  if ((pos_bits != PUV_QUANT_FP16 && (pos_bits < 1 || pos_bits > 16)) || attr_bits < 1 || attr_bits > 16)
+    return fail(PUV_E_INVALID_ARGUMENT, "bits (%d, %d) outside 1..16 (pos: or PUV_QUANT_FP16)", pos_bits, attr_bits);
   if (!codes && !proxy) return fail(PUV_E_INVALID_ARGUMENT, "codes and proxy are both NULL");
   const bool rho = layout->position_mode == PUV_POS_RHO;
   const int D = layout->planes;
@@ -583,7 +583,7 @@ puv_status puv_quantize(const puv_layout* layout, const float* const* atlas_plan
     if (codes && !codes[d]) return fail(PUV_E_INVALID_ARGUMENT, "code plane %d is NULL", d);
     if (proxy && !proxy[d]) return fail(PUV_E_INVALID_ARGUMENT, "proxy plane %d is NULL", d);
     x[d] = atlas_planes[d];
-    bits[d] = (int8_t)((d < 3) ? pos_bits : attr_bits);
+    bits[d] = (int8_t)((d < 3) ? (pos_bits == PUV_QUANT_FP16 ? -1 : pos_bits) : attr_bits);
   }
   { StageScope sc(PUV_STAGE_QUANT, (cudaStream_t)stream);
     puv::launch_quantize(x, proxy, codes, bits, D, spec, atlas_occ, (int64_t)layout->atlas_w * layout->atlas_h,

@@ -9,6 +9,8 @@
 //              t = ((x - min) / (max - min)) * L clamped to [0, L], code = roundf(t) (half away),
 //              proxy = min + (code / L) * (max - min); writes the codes (uint8 / uint16 planes,
 //              the storage format) and/or the fp32 proxy planes.
+#include <cuda_fp16.h>
+
 #include "contract.cuh"
 #include "internal.cuh"
 
@@ -85,10 +87,16 @@ struct QPlanes {
   const float* x[kMaxPlanes];
   float* proxy[kMaxPlanes];
   void* code[kMaxPlanes];
-  int8_t bits[kMaxPlanes];   // 0: plane not quantised (rho mode's unused planes 1, 2)
+  int8_t bits[kMaxPlanes];   // 0: plane not quantised (rho mode's unused planes 1, 2); -1: binary16
 };
 
 PUV_DEV void quant1(float x, float mn, float mx, int bits, uint32_t& code, float& prox) {
+  if (bits < 0) {   // reading Q8: IEEE binary16 (round to nearest even); code = its bit pattern
+    const __half h = __float2half_rn(x);
+    code = __half_as_ushort(h);
+    prox = __half2float(h);
+    return;
+  }
   code = 0;
   if (mx == mn) { prox = mn; return; }
   const float L = (float)((1u << bits) - 1u);
@@ -123,7 +131,7 @@ __global__ void __launch_bounds__(256) k_quantize4(QPlanes Q, int D, const float
       }
       if (Q.proxy[d]) __stcs(reinterpret_cast<float4*>(Q.proxy[d]) + i, make_float4(p[0], p[1], p[2], p[3]));
       if (Q.code[d]) {
-        if (bits > 8)
+        if (bits > 8 || bits < 0)
           reinterpret_cast<ushort4*>(Q.code[d])[i] = make_ushort4(c[0], c[1], c[2], c[3]);
         else
           reinterpret_cast<uchar4*>(Q.code[d])[i] = make_uchar4(c[0], c[1], c[2], c[3]);
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(256) k_quantize(QPlanes Q, int D, const float*
       if (on) quant1(__ldcs(Q.x[d] + i), smn[d], smx[d], bits, code, prox);
       if (Q.proxy[d]) Q.proxy[d][i] = prox;
       if (Q.code[d]) {
-        if (bits > 8) static_cast<uint16_t*>(Q.code[d])[i] = (uint16_t)code;
+        if (bits > 8 || bits < 0) static_cast<uint16_t*>(Q.code[d])[i] = (uint16_t)code;
         else static_cast<uint8_t*>(Q.code[d])[i] = (uint8_t)code;
       }
     }

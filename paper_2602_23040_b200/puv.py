@@ -319,9 +319,15 @@ def quant_fit(layout, atlas, occ, spec=None, stream=None):
     return spec
 
 
+QUANT_FP16 = 256   # pos_bits value: position planes stored as IEEE binary16 (include/puv.h, reading Q8)
+
+
 def quantize(layout, atlas, occ, spec, pos_bits=16, attr_bits=8, proxy=None, codes=False, stream=None):
     """LPO fake quantiser.  Returns (proxy (D, H_A, W_A) fp32 or None, code planes list or None); code
-    planes are uint8 (bits <= 8) or uint16 (bits > 8).  proxy=False skips the proxy."""
+    planes are uint8 (bits <= 8) or uint16 (bits > 8 or binary16).  proxy=False skips the proxy.
+    pos_bits="fp16" (or QUANT_FP16) stores the position planes as binary16."""
+    if pos_bits == "fp16":
+        pos_bits = QUANT_FP16
     dev = spec.device
     shp = (layout.atlas_h, layout.atlas_w)
     rho = layout.position_mode == POS_RHO
@@ -337,6 +343,7 @@ def quantize(layout, atlas, occ, spec, pos_bits=16, attr_bits=8, proxy=None, cod
         for d in range(layout.planes):
             bits = pos_bits if d < 3 else attr_bits
             code_list.append(torch.zeros(shp, dtype=torch.uint16 if bits > 8 else torch.uint8, device=dev))
+            # (QUANT_FP16 > 8: binary16 patterns are uint16 planes)
         ctab = _ptr_table(code_list)
     _ok(lib().puv_quantize(C.byref(layout), _planes(atlas), _ptr(occ), _ptr(spec), int(pos_bits), int(attr_bits),
                            ctab, ptab, _stream(stream)))

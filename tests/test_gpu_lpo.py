@@ -28,7 +28,8 @@ def _quant_check(layout, planes, occ, pos_bits=16, attr_bits=8, rho=False):
     skip = (1, 2) if rho else ()
     spec_ref = orc.quant_fit(planes, occ, skip=skip)
     assert np.array_equal(spec.cpu().numpy(), spec_ref)      # by value (+0 / -0 compare equal)
-    bits = [0 if d in skip else (pos_bits if d < 3 else attr_bits) for d in range(planes.shape[0])]
+    pb = orc.FP16 if pos_bits == "fp16" else pos_bits
+    bits = [0 if d in skip else (pb if d < 3 else attr_bits) for d in range(planes.shape[0])]
     codes_ref, proxy_ref = orc.quantize(planes, occ, spec_ref, bits)
     px = proxy.cpu().numpy()
     for d in range(planes.shape[0]):
@@ -46,7 +47,7 @@ def _quant_check(layout, planes, occ, pos_bits=16, attr_bits=8, rho=False):
     return spec, proxy, proxy_ref
 
 
-@pytest.mark.parametrize("pos_bits,attr_bits", [(16, 8), (12, 5), (8, 8), (16, 1)])
+@pytest.mark.parametrize("pos_bits,attr_bits", [(16, 8), (12, 5), (8, 8), (16, 1), ("fp16", 8)])
 def test_quantize_c2_bitexact(pos_bits, attr_bits):
     sc = make_scene(2)
     planes, occ, _ = orc.pack(sc.levels)
@@ -77,15 +78,17 @@ def test_quantize_degenerate_and_empty():
     assert spec.abs().max().item() == 0.0
 
 
-def test_lpo_render_forward_backward_c2():
+@pytest.mark.parametrize("pos_bits", [16, "fp16"])
+def test_lpo_render_forward_backward_c2(pos_bits):
     """C2, two views: render the GPU proxy; oracle renders its own (bit-identical) proxy; the backward
-    (STE) gradient lands on the master planes and matches the oracle's backward of the proxy."""
+    (STE) gradient lands on the master planes and matches the oracle's backward of the proxy.
+    pos_bits "fp16": positions stored as IEEE binary16 (reading Q8)."""
     sc = make_scene(2)
     views = [0, 9]
     dev = torch.device("cuda")
     planes, occ, _ = orc.pack(sc.levels)
     layout = puv.layout_for_levels([(lv.rows, lv.cols) for lv in sc.levels], sc.sh_degree)
-    spec, proxy, proxy_ref = _quant_check(layout, planes, occ)
+    spec, proxy, proxy_ref = _quant_check(layout, planes, occ, pos_bits=pos_bits)
     cams = puv.cameras([sc.cameras[v] for v in views])
     R = puv.Renderer(layout, cams, device=dev)
     O = torch.from_numpy(occ).to(dev)

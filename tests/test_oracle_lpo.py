@@ -82,3 +82,24 @@ def test_quantize_unoccupied_zero_and_passthrough():
     codes, proxy = orc.quantize(P, occ, spec, [16, 0, 8])
     assert np.all(codes[:, occ == 0] == 0) and np.all(proxy[0][occ == 0] == 0) and np.all(proxy[2][occ == 0] == 0)
     assert np.array_equal(proxy[1], P[1]) and np.all(codes[1] == 0)
+
+
+def test_fp16_positions_match_numpy_binary16():
+    """Reading Q8 (positions kept "in FP16"): the oracle's fp32 -> binary16 rounding
+    (bit fields written out in C) against numpy's float16 conversion (IEEE round to nearest even) on
+    every fp32 in [1, 2) (2^23 values, covering every mantissa rounding case incl. exact ties), a
+    log-uniform sweep over the whole range, subnormal halves, overflow and specials."""
+    rng = np.random.default_rng(3)
+    one_two = (np.arange(1 << 23, dtype=np.uint32) | np.uint32(0x3F800000)).view(np.float32)
+    sweep = (rng.choice([-1, 1], 2_000_000) * np.exp(rng.uniform(np.log(1e-9), np.log(1e6), 2_000_000))).astype(np.float32)
+    special = np.array([0.0, -0.0, 65504.0, 65519.99, 65520.0, 1e9, -1e9, np.inf, -np.inf, 2.0 ** -24, 2.0 ** -25,
+                        2.0 ** -25 * 1.0000001, 3 * 2.0 ** -26, 2.0 ** -14, 2.0 ** -14 * (1 - 2.0 ** -11),
+                        6.1e-5, 1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11], np.float32)
+    for x in (one_two, sweep, special, -one_two):
+        code, proxy = orc.fp16_bits(x)
+        with np.errstate(over="ignore"):
+            ref = x.astype(np.float16)
+        assert np.array_equal(code.astype(np.uint16), ref.view(np.uint16))
+        assert np.array_equal(proxy, ref.astype(np.float32))
+    nan_code, _ = orc.fp16_bits(np.array([np.nan], np.float32))
+    assert (nan_code[0] & 0x7C00) == 0x7C00 and (nan_code[0] & 0x3FF) != 0

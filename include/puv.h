@@ -376,6 +376,10 @@ typedef struct {
  * on the caller's stream instead of the internal binning streams, so every stage runs alone and
  * its per-stage event time (puv_profile_read) is its serialised cost.  Results are identical. */
 puv_status puv_profile_serial(int32_t on);
+/* The recorded stage instances since the last reset, in enqueue order (synchronises): per instance
+ * out[3i] = stage id, out[3i+1] / out[3i+2] = start / end in ms relative to the first instance's
+ * start (a timeline of the overlapped stages).  Host outputs; at most max_events instances. */
+puv_status puv_profile_timeline(double* out, int32_t max_events, int32_t* n_events);
 puv_status puv_profile_enable(int32_t on);
 puv_status puv_profile_read(puv_profile* out, int32_t reset);
 

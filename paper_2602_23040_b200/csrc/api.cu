@@ -910,6 +910,25 @@ puv_status puv_profile_enable(int32_t on) {
   return PUV_OK;
 }
 
+puv_status puv_profile_timeline(double* out, int32_t max_events, int32_t* n_events) {
+  if (!out || !n_events || max_events < 0) return fail(PUV_E_INVALID_ARGUMENT, "bad timeline arguments");
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int n = (int)g_prof_events.size() < max_events ? (int)g_prof_events.size() : max_events;
+  for (int i = 0; i < n; ++i) {
+    const ProfEvent& e = g_prof_events[i];
+    const cudaError_t err = cudaEventSynchronize(e.b);
+    if (err != cudaSuccess) return fail(PUV_E_CUDA, "puv_profile_timeline: %s", cudaGetErrorString(err));
+    float t0 = 0.f, t1 = 0.f;
+    cudaEventElapsedTime(&t0, g_prof_events[0].a, e.a);
+    cudaEventElapsedTime(&t1, g_prof_events[0].a, e.b);
+    out[3 * i] = e.stage;
+    out[3 * i + 1] = t0;
+    out[3 * i + 2] = t1;
+  }
+  *n_events = n;
+  return PUV_OK;
+}
+
 puv_status puv_profile_read(puv_profile* out, int32_t reset) {
   if (!out) return fail(PUV_E_INVALID_ARGUMENT, "NULL profile");
   std::memset(out, 0, sizeof *out);

@@ -17,9 +17,9 @@ constexpr int kNbMax = 1024;              // max key blocks of the stable tile p
 #endif
 constexpr int kBinStreams = PUV_BIN_STREAMS;  // views binned concurrently (one scratch block each)
 #ifndef PUV_BIN_PRIORITY
-#define PUV_BIN_PRIORITY 1
+#define PUV_BIN_PRIORITY 0
 #endif
-constexpr int kBinPriority = PUV_BIN_PRIORITY;  // binning streams at the highest stream priority
+constexpr int kBinPriority = PUV_BIN_PRIORITY;  // 1: binning streams at the highest priority (A/B: +2 ms/step, off)
 #ifndef PUV_DMASK
 #define PUV_DMASK 1
 #endif

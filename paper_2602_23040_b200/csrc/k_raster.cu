@@ -24,7 +24,7 @@ namespace puv {
 constexpr int kFwdPPT = PUV_FWD_PPT;                     // pixels per thread (one column, rows r + 4k)
 constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128 (PPT 2) or 64 (PPT 4)
 #ifndef PUV_FWD_MINB
-#define PUV_FWD_MINB 0
+#define PUV_FWD_MINB 7
 #endif
 #if PUV_FWD_MINB > 0
 #define PUV_FWD_BOUNDS __launch_bounds__(kTile * kTile / PUV_FWD_PPT, PUV_FWD_MINB)
@@ -35,6 +35,45 @@ constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128 (PPT 2) or 64 (P
 #define PUV_FWD_BATCH 128
 #endif
 constexpr int kFwdBatch = PUV_FWD_BATCH;                 // entries staged per batch
+
+#ifndef PUV_FWD_CULL
+#define PUV_FWD_CULL 1
+#endif
+
+// Conservative per-warp entry filter (not a decision: every composited pair is still decided by the
+// contract's per-pixel skip test R1).  Can any pixel centre (i, j) of the block i in [x0, x0 + 7],
+// j in [y0, y0 + 7] reach power = ha dx^2 + nb dx dy + hc dy^2 >= t_g ((dx, dy) = mean - pixel)?
+// The quadratic is concave (the conic of Sigma2D + 0.3 I), so its maximum over the box is 0 if the
+// mean lies inside, else the largest of the four edge maxima (each a clamped 1-D vertex).  Kept
+// when that maximum is >= t_g - margin, the margin (1e-3 of the terms' magnitude bound over the
+// box + 1e-4) dwarfing the fp32 rounding of both this test and the contract's power: an entry
+// whose pairs could pass R1 somewhere in the block is never dropped.
+__device__ __forceinline__ bool block_may_hit(float mx, float my, float ha, float nb, float hc, float tg, float x0,
+                                              float y0, float ext) {
+  const float dxl = mx - (x0 + ext), dxh = mx - x0, dyl = my - (y0 + ext), dyh = my - y0;
+  if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return tg <= 0.f;
+  const float dxm = fmaxf(fabsf(dxl), fabsf(dxh)), dym = fmaxf(fabsf(dyl), fabsf(dyh));
+  const float margin = 1e-3f * (fabsf(ha) * dxm * dxm + fabsf(nb) * dxm * dym + fabsf(hc) * dym * dym) + 1e-4f;
+  const float ihc = -0.5f / hc, iha = -0.5f / ha;   // vertex of q along y (resp. x): d* = -nb e / (2 hc)
+  float best = -INFINITY;
+  {
+    const float dy = fminf(fmaxf(nb * dxl * ihc, dyl), dyh);
+    best = fmaxf(best, dxl * (ha * dxl + nb * dy) + hc * dy * dy);
+  }
+  {
+    const float dy = fminf(fmaxf(nb * dxh * ihc, dyl), dyh);
+    best = fmaxf(best, dxh * (ha * dxh + nb * dy) + hc * dy * dy);
+  }
+  {
+    const float dx = fminf(fmaxf(nb * dyl * iha, dxl), dxh);
+    best = fmaxf(best, dx * (ha * dx + nb * dyl) + hc * dyl * dyl);
+  }
+  {
+    const float dx = fminf(fmaxf(nb * dyh * iha, dxl), dxh);
+    best = fmaxf(best, dx * (ha * dx + nb * dyh) + hc * dyh * dyh);
+  }
+  return best >= tg - margin;
+}
 
 template <int P>
 __device__ __forceinline__ bool all_of(const bool (&b)[P]) {
@@ -116,7 +155,35 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
     }
     __syncthreads();
     const int n = __all_sync(0xffffffffu, all_of(done)) ? 0 : (int)min((uint32_t)kFwdBatch, end - b0);
+#if PUV_FWD_CULL
+    // per-warp filter: one box test per staged entry (lanes split the batch), ballots -> the
+    // entries whose ellipse can reach this warp's 8x8 block; the walk visits only those (the
+    // skipped ones get their all-zero K6 mask words here)
+    static_assert(kFwdBatch % 32 == 0 && kFwdBatch <= 128, "batch = 1..4 words of entry bits");
+    uint32_t mwords[kFwdBatch / 32];
+    {
+      const float bx0 = (float)(tx * kTile + (warp & 1) * 8), by0 = (float)(ty * kTile + (warp >> 1) * 4 * kFwdPPT);
+#pragma unroll
+      for (int q = 0; q < kFwdBatch / 32; ++q) {
+        const int j = 32 * q + lane;
+        bool may = false;
+        if (j < n) {
+          const float4 A = sA[j];
+          const float4 B = sB[j];
+          may = block_may_hit(A.x, A.y, A.z, A.w, B.x, B.y, bx0, by0, (float)(4 * kFwdPPT - 1));
+          const uint32_t e = b0 + j - start;
+          if (!may && kMaskCap > 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(0u, 0u);
+        }
+        mwords[q] = __ballot_sync(0xffffffffu, may);
+      }
+    }
+    bool stop = false;
+    for (int q = 0; q < kFwdBatch / 32 && !stop; ++q)
+    for (uint32_t bits = mwords[q]; bits; bits &= bits - 1) {
+      const int j = 32 * q + __ffs(bits) - 1;
+#else
     for (int j = 0; j < n; ++j) {
+#endif
       const float4 A = sA[j];
       const float4 B = sB[j];
       bool hit[kFwdPPT];
@@ -166,7 +233,12 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         const uint32_t m0 = __ballot_sync(0xffffffffu, comp[0]), m1 = __ballot_sync(0xffffffffu, comp[1]);
         if (lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(m0, m1);
       }
-      if (__all_sync(0xffffffffu, all_of(done))) break;
+      if (__all_sync(0xffffffffu, all_of(done))) {
+#if PUV_FWD_CULL
+        stop = true;
+#endif
+        break;
+      }
     }
   }
   uint32_t n_exam = 0;

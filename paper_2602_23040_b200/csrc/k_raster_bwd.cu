@@ -21,6 +21,8 @@
 // pixels' fp64 chains interleave.  A thread sums the 9 moments of an entry over its pixels; the
 // warp sums them with a transposing shuffle butterfly and 9 lanes issue one fp64 atomic
 // each into the (view, Gaussian) slot.
+#include <type_traits>
+
 #include "contract.cuh"
 #include "internal.cuh"
 
@@ -40,6 +42,9 @@ namespace puv {
 constexpr int kBwdPPT = PUV_BWD_PPT;                       // pixels per thread (one column, rows r + 4k)
 constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128 (PPT 2) or 64 (PPT 4)
 constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4-bank skew per row
+#ifndef PUV_BWD_CAPSPLIT
+#define PUV_BWD_CAPSPLIT 1
+#endif
 #ifndef PUV_BWD_BATCH
 #define PUV_BWD_BATCH 64
 #endif
@@ -239,26 +244,37 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       const double hadxx = d1.x * dxx, nbdx = d1.y * dx;
       double gv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // Mx, My, Mxx, Mxy, Myy, sum GdL, colour r, g, b
       double sdy = 0.0;                              // sum GdL dy (-> Mxy = dx sdy)
+      // The pixel bodies, compiled twice: the alpha-cap selects exist only in the (warp-uniform,
+      // rare: o >= 0.99) capped variant, so the common path carries no cap logic at all.
+      auto bodies = [&](auto cap_tag) {
+        constexpr bool kCap = decltype(cap_tag)::value;
 #pragma unroll
-      for (int k = 0; k < kBwdPPT; ++k) {
-        const double dy = d0.y - dj[k];
-        const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
-        double a = act[k] ? o * G : 0.0;
-        if (__builtin_expect(may_cap, 0)) a = cap[k] ? 0.99 : a;     // warp-uniform, rare
-        const double aT = a * T[k];
-        const double cd = fma(dC[k][0], d3.x, fma(dC[k][1], d3.y, dC[k][2] * cb));
-        Sd[k] = fma(-cd, aT, Sd[k]);
-        const double dLda = fma(cd, T[k], -Sd[k] * rcp64(1.0 - a));
-        gv[6] = fma(aT, dC[k][0], gv[6]);
-        gv[7] = fma(aT, dC[k][1], gv[7]);
-        gv[8] = fma(aT, dC[k][2], gv[8]);
-        double GdL = act[k] ? G * dLda : 0.0;
-        if (__builtin_expect(may_cap, 0)) GdL = cap[k] ? 0.0 : GdL;  // capped: no gradient through alpha
-        gv[5] += GdL;
-        sdy = fma(GdL, dy, sdy);
-        gv[4] = fma(GdL * dy, dy, gv[4]);
-        T[k] -= aT;                                          // T_{k+1} = T_k (1 - a_k)
-      }
+        for (int k = 0; k < kBwdPPT; ++k) {
+          const double dy = d0.y - dj[k];
+          const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
+          double a = act[k] ? o * G : 0.0;
+          if (kCap) a = cap[k] ? 0.99 : a;
+          const double aT = a * T[k];
+          const double cd = fma(dC[k][0], d3.x, fma(dC[k][1], d3.y, dC[k][2] * cb));
+          Sd[k] = fma(-cd, aT, Sd[k]);
+          const double dLda = fma(cd, T[k], -Sd[k] * rcp64(1.0 - a));
+          gv[6] = fma(aT, dC[k][0], gv[6]);
+          gv[7] = fma(aT, dC[k][1], gv[7]);
+          gv[8] = fma(aT, dC[k][2], gv[8]);
+          double GdL = act[k] ? G * dLda : 0.0;
+          if (kCap) GdL = cap[k] ? 0.0 : GdL;   // capped: no gradient through alpha
+          gv[5] += GdL;
+          sdy = fma(GdL, dy, sdy);
+          gv[4] = fma(GdL * dy, dy, gv[4]);
+          T[k] -= aT;                             // T_{k+1} = T_k (1 - a_k)
+        }
+      };
+#if PUV_BWD_CAPSPLIT
+      if (__builtin_expect(may_cap, 0)) bodies(std::true_type{});
+      else bodies(std::false_type{});
+#else
+      bodies(std::true_type{});   // (A/B reference: one body with the cap selects; cap[] is all-false unless may_cap)
+#endif
       gv[0] = dx * gv[5];
       gv[1] = sdy;
       gv[2] = dxx * gv[5];

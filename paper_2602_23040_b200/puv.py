@@ -131,6 +131,8 @@ def lib():
         L.puv_quantize.restype = C.c_int32
         L.puv_profile_enable.argtypes = [S]
         L.puv_profile_serial.argtypes = [S]
+        L.puv_profile_timeline.argtypes = [P, S, P]
+        L.puv_profile_timeline.restype = C.c_int32
         L.puv_profile_serial.restype = C.c_int32
         L.puv_profile_read.argtypes = [P, S]
         L.puv_profile_enable.restype = C.c_int32
@@ -506,6 +508,14 @@ def debug_view(layout, cams, state, arena, view, stream=None) -> ViewDebug:
 def profile_serial(on: bool = True):
     """Run each view's depth sort + binning on the caller's stream (serialised stage times)."""
     _ok(lib().puv_profile_serial(1 if on else 0))
+
+
+def profile_timeline(max_events: int = 100000):
+    """[(stage name, start ms, end ms)] of the recorded stage instances (call before profile_read(reset))."""
+    buf = (C.c_double * (3 * max_events))()
+    n = C.c_int32()
+    _ok(lib().puv_profile_timeline(buf, max_events, C.byref(n)))
+    return [(STAGES[int(buf[3 * i])], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
 
 
 def profile_enable(on: bool = True):

@@ -118,4 +118,39 @@ PUV_DEV double rcp64(double y) {
   return fma(r, e, r);
 }
 
+// Conservative per-warp entry filter of K5/K6 (not part of the contract and not a decision: every
+// composited pair is still decided by the per-pixel skip test R1).  Can any pixel centre (i, j) of
+// the block i in [x0, x0 + ex], j in [y0, y0 + ey] reach power = ha dx^2 + nb dx dy + hc dy^2 >= t_g ((dx, dy) = mean - pixel)?
+// The quadratic is concave (the conic of Sigma2D + 0.3 I), so its maximum over the box is 0 if the
+// mean lies inside, else the largest of the four edge maxima (each a clamped 1-D vertex).  Kept
+// when that maximum is >= t_g - margin, the margin (1e-3 of the terms' magnitude bound over the
+// box + 1e-4) dwarfing the fp32 rounding of both this test and the contract's power: an entry
+// whose pairs could pass R1 somewhere in the block is never dropped.
+__device__ __forceinline__ bool block_may_hit(float mx, float my, float ha, float nb, float hc, float tg, float x0,
+                                              float y0, float ex, float ey) {
+  const float dxl = mx - (x0 + ex), dxh = mx - x0, dyl = my - (y0 + ey), dyh = my - y0;
+  if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return tg <= 0.f;
+  const float dxm = fmaxf(fabsf(dxl), fabsf(dxh)), dym = fmaxf(fabsf(dyl), fabsf(dyh));
+  const float margin = 1e-3f * (fabsf(ha) * dxm * dxm + fabsf(nb) * dxm * dym + fabsf(hc) * dym * dym) + 1e-4f;
+  const float ihc = -0.5f / hc, iha = -0.5f / ha;   // vertex of q along y (resp. x): d* = -nb e / (2 hc)
+  float best = -INFINITY;
+  {
+    const float dy = fminf(fmaxf(nb * dxl * ihc, dyl), dyh);
+    best = fmaxf(best, dxl * (ha * dxl + nb * dy) + hc * dy * dy);
+  }
+  {
+    const float dy = fminf(fmaxf(nb * dxh * ihc, dyl), dyh);
+    best = fmaxf(best, dxh * (ha * dxh + nb * dy) + hc * dy * dy);
+  }
+  {
+    const float dx = fminf(fmaxf(nb * dyl * iha, dxl), dxh);
+    best = fmaxf(best, dx * (ha * dx + nb * dyl) + hc * dyl * dyl);
+  }
+  {
+    const float dx = fminf(fmaxf(nb * dyh * iha, dxl), dxh);
+    best = fmaxf(best, dx * (ha * dx + nb * dyh) + hc * dyh * dyh);
+  }
+  return best >= tg - margin;
+}
+
 }  // namespace puv

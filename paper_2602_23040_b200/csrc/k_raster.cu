@@ -36,44 +36,12 @@ constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128 (PPT 2) or 64 (P
 #endif
 constexpr int kFwdBatch = PUV_FWD_BATCH;                 // entries staged per batch
 
+#ifndef PUV_FWD_BRANCHFREE
+#define PUV_FWD_BRANCHFREE 0
+#endif
 #ifndef PUV_FWD_CULL
 #define PUV_FWD_CULL 1
 #endif
-
-// Conservative per-warp entry filter (not a decision: every composited pair is still decided by the
-// contract's per-pixel skip test R1).  Can any pixel centre (i, j) of the block i in [x0, x0 + 7],
-// j in [y0, y0 + 7] reach power = ha dx^2 + nb dx dy + hc dy^2 >= t_g ((dx, dy) = mean - pixel)?
-// The quadratic is concave (the conic of Sigma2D + 0.3 I), so its maximum over the box is 0 if the
-// mean lies inside, else the largest of the four edge maxima (each a clamped 1-D vertex).  Kept
-// when that maximum is >= t_g - margin, the margin (1e-3 of the terms' magnitude bound over the
-// box + 1e-4) dwarfing the fp32 rounding of both this test and the contract's power: an entry
-// whose pairs could pass R1 somewhere in the block is never dropped.
-__device__ __forceinline__ bool block_may_hit(float mx, float my, float ha, float nb, float hc, float tg, float x0,
-                                              float y0, float ext) {
-  const float dxl = mx - (x0 + ext), dxh = mx - x0, dyl = my - (y0 + ext), dyh = my - y0;
-  if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return tg <= 0.f;
-  const float dxm = fmaxf(fabsf(dxl), fabsf(dxh)), dym = fmaxf(fabsf(dyl), fabsf(dyh));
-  const float margin = 1e-3f * (fabsf(ha) * dxm * dxm + fabsf(nb) * dxm * dym + fabsf(hc) * dym * dym) + 1e-4f;
-  const float ihc = -0.5f / hc, iha = -0.5f / ha;   // vertex of q along y (resp. x): d* = -nb e / (2 hc)
-  float best = -INFINITY;
-  {
-    const float dy = fminf(fmaxf(nb * dxl * ihc, dyl), dyh);
-    best = fmaxf(best, dxl * (ha * dxl + nb * dy) + hc * dy * dy);
-  }
-  {
-    const float dy = fminf(fmaxf(nb * dxh * ihc, dyl), dyh);
-    best = fmaxf(best, dxh * (ha * dxh + nb * dy) + hc * dy * dy);
-  }
-  {
-    const float dx = fminf(fmaxf(nb * dyl * iha, dxl), dxh);
-    best = fmaxf(best, dx * (ha * dx + nb * dyl) + hc * dyl * dyl);
-  }
-  {
-    const float dx = fminf(fmaxf(nb * dyh * iha, dxl), dxh);
-    best = fmaxf(best, dx * (ha * dx + nb * dyh) + hc * dyh * dyh);
-  }
-  return best >= tg - margin;
-}
 
 template <int P>
 __device__ __forceinline__ bool all_of(const bool (&b)[P]) {
@@ -170,7 +138,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         if (j < n) {
           const float4 A = sA[j];
           const float4 B = sB[j];
-          may = block_may_hit(A.x, A.y, A.z, A.w, B.x, B.y, bx0, by0, (float)(4 * kFwdPPT - 1));
+          may = block_may_hit(A.x, A.y, A.z, A.w, B.x, B.y, bx0, by0, 7.f, (float)(4 * kFwdPPT - 1));
           const uint32_t e = b0 + j - start;
           if (!may && kMaskCap > 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(0u, 0u);
         }
@@ -204,6 +172,31 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
       const double d4x = sD[4][j].x;
       const double dx = d0.x - di;
       const double hadxx = d1.x * (dx * dx), nbdx = d1.y * dx;
+#if PUV_FWD_BRANCHFREE
+      // both pixels' bodies run under selects (no divergent branches): the contract on a safe
+      // argument (power 0) where the pixel did not hit, every state update gated by its flags
+#pragma unroll
+      for (int k = 0; k < kFwdPPT; ++k) {
+        const float ao = mul(B.z, exp_c_core(hit[k] ? power[k] : 0.0f));
+        const bool capped = !(ao < 0.99f);
+        const float alpha = capped ? 0.99f : ao;
+        const float Tn = mul(T[k], sub(1.0f, alpha));
+        const bool term = hit[k] && Tn < 1e-4f;
+        comp[k] = hit[k] && !term;
+        exam[k] = term ? e + 1 : exam[k];
+        done[k] = done[k] || term;
+        T[k] = comp[k] ? Tn : T[k];
+        last[k] = comp[k] ? e + 1 : last[k];
+        n_comp += comp[k] ? 1u : 0u;
+        const double pw = power64(d2.x, hadxx, nbdx, d0.y - dj[k]);
+        const double a64 = capped ? 0.99 : d2.y * exp64(fmax(pw, -700.0), sExp);
+        const double w = comp[k] ? a64 * T64[k] : 0.0;
+        C[k][0] = fma(d3.x, w, C[k][0]);
+        C[k][1] = fma(d3.y, w, C[k][1]);
+        C[k][2] = fma(d4x, w, C[k][2]);
+        T64[k] -= w;   // T64 * (1 - a64)
+      }
+#else
 #pragma unroll
       for (int k = 0; k < kFwdPPT; ++k) {
         if (!hit[k]) continue;
@@ -229,6 +222,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         C[k][2] = fma(d4x, w, C[k][2]);
         T64[k] -= w;   // T64 * (1 - a64)
       }
+#endif
       if (kMaskCap > 0) {
         const uint32_t m0 = __ballot_sync(0xffffffffu, comp[0]), m1 = __ballot_sync(0xffffffffu, comp[1]);
         if (lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(m0, m1);

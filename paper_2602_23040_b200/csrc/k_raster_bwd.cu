@@ -42,6 +42,9 @@ namespace puv {
 constexpr int kBwdPPT = PUV_BWD_PPT;                       // pixels per thread (one column, rows r + 4k)
 constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128 (PPT 2) or 64 (PPT 4)
 constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4-bank skew per row
+#ifndef PUV_BWD_CULL
+#define PUV_BWD_CULL 1
+#endif
 #ifndef PUV_BWD_CAPSPLIT
 #define PUV_BWD_CAPSPLIT 1
 #endif
@@ -193,9 +196,38 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       }
     }
     __syncthreads();
+#if PUV_BWD_CULL
+    // per-warp entry filter: an entry is walked only if some pixel of this warp may composite it --
+    // K5's composited-pixel words of the warp are nonzero (first kMaskCap entries; stale words past
+    // a pixel's end only keep an entry, never drop one), or, beyond the mask, the conservative
+    // ellipse-vs-block test of K5 for the warp's 8 x 16 pixels
+    uint32_t mwords[kBwdBatch / 32];
+#pragma unroll
+    for (int q = 0; q < kBwdBatch / 32; ++q) {
+      const int j = 32 * q + lane;
+      bool may = false;
+      if (j < n && lo + j < wlast) {
+        if (lo + j < (uint32_t)kMaskCap) {
+          const uint4 w = sM[j][warp];
+          may = (w.x | w.y | w.z | w.w) != 0u;
+        } else {
+          const float4 A = sA[j];
+          const float4 B = sB[j];
+          may = block_may_hit(A.x, A.y, A.z, A.w, B.x, B.y, (float)(tx * kTile + (warp & 1) * 8),
+                              (float)(ty * kTile + (warp >> 1) * 4 * kBwdPPT), 7.f, (float)(4 * kBwdPPT - 1));
+        }
+      }
+      mwords[q] = __ballot_sync(0xffffffffu, may);
+    }
+    static_assert(kBwdBatch == 64, "the walk keeps the batch's entry bits in one 64-bit word");
+    for (uint64_t bits = ((uint64_t)mwords[1] << 32) | mwords[0]; bits; bits &= bits - 1) {
+      const int j = __ffsll((long long)bits) - 1;
+      const uint32_t e = lo + j;
+#else
     for (int j = 0; j < n; ++j) {
       const uint32_t e = lo + j;
       if (e >= wlast) break;  // warp-uniform: no pixel of this warp reaches entry e
+#endif
       const float4 B = sB[j];
       // decisions (fp32 contract), per pixel: the first kMaskCap entries from K5's composited
       // bits (bit = composited at this entry; guarded by e < last since K5 writes a warp's words

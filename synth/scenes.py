@@ -318,6 +318,30 @@ def motion_masks(scene: Scene, views, n_blobs=6, rmin=0.03, rmax=0.12, tag=2) ->
     return out
 
 
+def moving_region_masks(scene: Scene, views, centre, radius, tag=4) -> np.ndarray:
+    """Seeded stand-in for thresholded + dilated optical-flow masks of a spatially coherent motion
+    (PAPER.md:362-378): the moving part of the scene is the ball |x - centre| <= radius; in every
+    view its mask is the image disc the ball projects to (centre projected, angular radius
+    asin(radius / distance)), so only Gaussians that overlap the moving region in some camera can
+    be labelled dynamic.  Returns (len(views), H, W) uint8 in {0, 1}."""
+    cam0 = scene.cameras[views[0]]
+    H, W = cam0.height, cam0.width
+    out = np.zeros((len(views), H, W), np.uint8)
+    jj, ii = np.mgrid[0:H, 0:W]
+    c = np.asarray(centre, np.float64)
+    for k, v in enumerate(views):
+        cam = scene.cameras[v]
+        V = cam.viewmat.astype(np.float64)
+        p = V[:3, :3] @ c + V[:3, 3]
+        if p[2] <= radius:
+            out[k] = 1          # the camera is inside / behind the ball's near side: all pixels move
+            continue
+        u, w_ = cam.fx * p[0] / p[2] + cam.cx, cam.fy * p[1] / p[2] + cam.cy
+        r_px = cam.fx * math.tan(math.asin(min(1.0, radius / float(np.linalg.norm(p)))))
+        out[k][(ii - u) ** 2 + (jj - w_) ** 2 <= r_px * r_px] = 1
+    return out
+
+
 # ----------------------------------------------------------------------------
 # tiny hand-built scenes for pins (tests)
 

@@ -21,10 +21,13 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2602_23040_b200 import puv  # noqa: E402
-from synth.scenes import make_scene, motion_masks, ring, rho_scene  # noqa: E402
+from synth.scenes import make_scene, motion_masks, moving_region_masks, ring, rho_scene  # noqa: E402
 
 
-def bench_label(steps=5, warmup=2):
+def bench_label(steps=5, warmup=2, region=True):
+    """region=True: the motion masks of a spatially coherent moving part (a 0.6 m ball around the
+    scene point nearest to the densest texel neighbourhood, synth.moving_region_masks); False: the
+    round-1 seeded disc masks (unstructured: their OR over 55 cameras labels ~97 % dynamic)."""
     sc = make_scene(4)
     dev = torch.device("cuda")
     lv = sc.levels[0]
@@ -32,7 +35,18 @@ def bench_label(steps=5, warmup=2):
     atlas = torch.from_numpy(lv.planes).to(dev)
     occ = torch.from_numpy(lv.occ).to(dev)
     cams = puv.cameras(sc.cameras)
-    masks = torch.from_numpy(motion_masks(sc, list(range(len(sc.cameras))))).to(dev)
+    if region:
+        mu = lv.planes[0:3].reshape(3, -1).T
+        rng = np.random.default_rng(np.random.SeedSequence([2602, 23040, 4, 5]))
+        cand = mu[rng.choice(mu.shape[0], 64, replace=False)]
+        # the candidate with the most texels within 0.6 m: a moving part inside one of the blobs
+        counts = [(np.linalg.norm(mu[::16] - c, axis=1) <= 0.6).sum() for c in cand]
+        centre, radius = cand[int(np.argmax(counts))], 0.6
+        masks_np = moving_region_masks(sc, list(range(len(sc.cameras))), centre, radius)
+        inside = float((np.linalg.norm(mu - centre, axis=1) <= radius).mean())
+    else:
+        masks_np = motion_masks(sc, list(range(len(sc.cameras))))
+    masks = torch.from_numpy(masks_np).to(dev)
     ws = torch.empty(puv.label_workspace_bytes(cams[0].width, cams[0].height), dtype=torch.uint8, device=dev)
     labels = torch.empty((lv.rows, lv.cols), dtype=torch.uint8, device=dev)
     for _ in range(warmup):
@@ -53,7 +67,10 @@ def bench_label(steps=5, warmup=2):
             "dynamic_fraction": float(labels.float().mean().item()),
             "mask_fraction": float(masks.float().mean().item()),
             "gpu_launches_per_call": (puv.kernel_launches() - l0) // steps,
-            "workload": "C4 atlas 1024^2 SH3, 55 dome cameras 1920x1080, seeded disc motion masks"}
+            "moving_ball_fraction": inside if region else None,
+            "workload": "C4 atlas 1024^2 SH3, 55 dome cameras 1920x1080, " +
+                        ("masks of a moving 0.6 m ball (synth.moving_region_masks)" if region else
+                         "seeded disc motion masks")}
 
 
 def _time_steps(R, planes, occ, targets, steps, warmup):

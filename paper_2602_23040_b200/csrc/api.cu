@@ -222,7 +222,7 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.view_hdr = take(sizeof(ViewHdr) * V);
   p.depth = take(4 * V * N);
   p.rect = take(8 * V * N);
-  p.rec = take(48 * V * N);
+  p.rec = take(32 * V * N);
   p.rec64 = take(80 * V * N);
   p.grad2d = take(72 * V * N);
   p.sorted = take(4 * V * N);

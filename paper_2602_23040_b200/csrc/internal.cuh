@@ -93,12 +93,12 @@ struct Plan {
 };
 
 // Records of a visible (view, Gaussian):
-//  rec   (fp32 contract, 48 B): A=(mx,my,ha,nb) B=(hc,t_g,o,-) C=(r,g,b,flags)   -> decisions + forward image
+//  rec   (fp32 contract, 32 B): A=(mx,my,ha,nb) B=(hc,t_g,o,flags)  -> every decision; flags = SH clamp bits (K7)
 //  rec64 (fp64 values,   80 B): (mx,my) (ha,nb) (hc,o) (r,g) (b,-)               -> backward values
 struct Views {
   uint32_t* depth;   // [V][N]
   uint2* rect;       // [V][N]  (x0 | x1<<16, y0 | y1<<16)
-  float4* rec;       // [V][N][3]
+  float4* rec;       // [V][N][2]
   double2* rec64;    // [V][N][5]
   double* grad2d;    // [V][N][9]  d/d(mx,my,ha,nb,hc,o,r,g,b), fp64
   uint32_t* sorted;  // [V][N]  gids in (depth, gid) order, first n_vis valid

@@ -3,9 +3,9 @@
 // One thread per texel; the texel's planes are read ONCE (coalesced SoA loads)
 // and the thread loops over up to kCamBatch views.  Per visible (view, Gaussian)
 // it writes: the depth key and tile rect (fp32 contract, R13 -> binning), the
-// 48-byte fp32 record (contract conic/mean/t_g/o + colour -> forward raster and
-// every compositing decision) and the 80-byte fp64 value record (the same
-// quantities in double -> backward).  The (view, Gaussian) 2D-gradient slots
+// 32-byte fp32 record (contract conic/mean/t_g/o -> every compositing decision, and
+// the SH clamp bits for K7) and the 80-byte fp64 value record (mean, conic, o and
+// colour in double -> the composited values of K5 and K6): 124 B.  The (view, Gaussian) 2D-gradient slots
 // K6 accumulates into are zeroed by the backward call itself (re-entrant backward).
 #include "project.cuh"
 
@@ -72,10 +72,9 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
       if (rgb[ch] < 0.0) { rgb[ch] = 0.0; flags |= 1u << ch; }
     v.depth[o] = pr.depth_bits;
     v.rect[o] = make_uint2((uint32_t)pr.x0 | ((uint32_t)pr.x1 << 16), (uint32_t)pr.y0 | ((uint32_t)pr.y1 << 16));
-    float4* rec = v.rec + 3 * o;
+    float4* rec = v.rec + 2 * o;
     rec[0] = make_float4(pr.mx, pr.my, pr.ha, pr.nb);
-    rec[1] = make_float4(pr.hc, u.t_g, u.o, 0.0f);
-    rec[2] = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], __uint_as_float(flags));
+    rec[1] = make_float4(pr.hc, u.t_g, u.o, __uint_as_float(flags));
     double2* r64 = v.rec64 + 5 * o;
     r64[0] = make_double2(p64.mx, p64.my);
     r64[1] = make_double2(p64.ha, p64.nb);

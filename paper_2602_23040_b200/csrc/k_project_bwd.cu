@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(PlaneTab P, PosMode pm, con
     dmu2 += (double)c.V[2] * dpx + (double)c.V[6] * dpy + (double)c.V[10] * dpz;
     dop += dO;
     // colour
-    const uint32_t flags = __float_as_uint(v.rec[3 * o + 2].w);
+    const uint32_t flags = __float_as_uint(v.rec[2 * o + 1].w);
     const double drgb[3] = {(flags & 1u) ? 0.0 : dr, (flags & 2u) ? 0.0 : dg, (flags & 4u) ? 0.0 : db_};
     double ex = mux - (double)c.campos[0], ey = muy - (double)c.campos[1], ez = muz - (double)c.campos[2];
     const double dist = sqrt(ex * ex + ey * ey + ez * ez), idist = 1.0 / dist;

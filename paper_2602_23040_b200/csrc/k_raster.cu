@@ -79,7 +79,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
     end = v.tend[(size_t)view * ntiles + tile];
   }
   const uint32_t* list = arena + hdr.list_base;
-  const float4* rec = v.rec + (size_t)view * N * 3;
+  const float4* rec = v.rec + (size_t)view * N * 2;
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   const float fi = (float)px;
   const double di = px;
@@ -115,8 +115,8 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
       if (idx < end) {
         const uint32_t g = list[idx];
         PUV_CHECK(g < (uint32_t)N && idx < hdr.K);
-        sA[i] = rec[3 * (size_t)g + 0];
-        sB[i] = rec[3 * (size_t)g + 1];
+        sA[i] = rec[2 * (size_t)g + 0];
+        sB[i] = rec[2 * (size_t)g + 1];
 #pragma unroll
         for (int k = 0; k < 5; ++k) sD[k][i] = rec64[5 * (size_t)g + k];
       }

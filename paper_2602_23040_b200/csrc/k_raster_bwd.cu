@@ -135,7 +135,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
   if (hdr.overflow) return;
   const uint32_t start = v.tstart[(size_t)view * ntiles + tile];
   const uint32_t* list = arena + hdr.list_base + start;
-  const float4* rec = v.rec + (size_t)view * N * 3;
+  const float4* rec = v.rec + (size_t)view * N * 2;
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   double* g2 = v.grad2d + (size_t)view * N * 9;
   const size_t HW = (size_t)W * H;
@@ -185,8 +185,8 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       const uint32_t g = list[lo + i];
       PUV_CHECK(g < (uint32_t)N && start + lo + i < hdr.K);
       sG[i] = g;
-      sA[i] = rec[3 * (size_t)g + 0];
-      sB[i] = rec[3 * (size_t)g + 1];
+      sA[i] = rec[2 * (size_t)g + 0];
+      sB[i] = rec[2 * (size_t)g + 1];
 #pragma unroll
       for (int k = 0; k < 5; ++k) sD[k][i] = rec64[5 * (size_t)g + k];
       if (lo + i < (uint32_t)kMaskCap) {

@@ -16,7 +16,10 @@
 namespace puv {
 
 template <int DEG>
-__global__ void __launch_bounds__(128) k_project_bwd(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ,
+#ifndef PUV_PBWD_MINB
+#define PUV_PBWD_MINB 1
+#endif
+__global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ,
                                                     const uint8_t* __restrict__ mask, int N,
                                                     const __grid_constant__ CamBatch cb, Views v, GradTab Gt) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;

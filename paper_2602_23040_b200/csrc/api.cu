@@ -102,9 +102,9 @@ static StreamSet& stream_set(int /*n*/) {
   if ((int)sets.size() <= dev) sets.resize(dev + 1, nullptr);
   if (!sets[dev]) {
     StreamSet* ss = new StreamSet();
-    // The binning streams run at the device's highest stream priority: their kernels are small and
-    // latency bound, and the compositing of the previous view (a full-GPU grid on the caller's
-    // stream) must not starve them, or the next view's compositing waits for its tile lists.
+    // Binning streams at the highest stream priority only with -DPUV_BIN_PRIORITY=1: the step is
+    // SM-time bound, and prioritised binning slows the compositing by more than it removes from the
+    // composite waits (A/B on one B200: +2 ms per C3 step).
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     for (int i = 0; i < kBinStreams; ++i)
@@ -785,17 +785,18 @@ puv_status puv_train_step_host(const puv_layout* layout, const float* const* atl
   cudaEvent_t fork = nullptr, done = nullptr;
   cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  // the uploads first, alone on the host link (K1 needs all of them); then the targets on the copy
+  // stream, overlapping K1 and the render (the first loss waits for them)
+  for (int i = 0; i < n_uploads; ++i)
+    if (uploads[i].bytes) cudaMemcpyAsync(uploads[i].dst, uploads[i].src, uploads[i].bytes, cudaMemcpyHostToDevice, s);
   {
     std::lock_guard<std::mutex> lock(ss.mu);   // the copy stream is shared per device
-    // targets on the copy stream (after earlier work on `s` released the buffer), overlapping the render
-    cudaEventRecord(fork, s);
+    cudaEventRecord(fork, s);                  // also orders the target buffer after earlier work on `s`
     cudaStreamWaitEvent(ss.cp, fork, 0);
     cudaMemcpyAsync(targets, targets_host, (size_t)n_views * 3 * W * H * sizeof(float), cudaMemcpyHostToDevice,
                     ss.cp);
     cudaEventRecord(done, ss.cp);
   }
-  for (int i = 0; i < n_uploads; ++i)
-    if (uploads[i].bytes) cudaMemcpyAsync(uploads[i].dst, uploads[i].src, uploads[i].bytes, cudaMemcpyHostToDevice, s);
   st = train_step_enqueue(layout, atlas_planes, atlas_occ, n_views, cams, opts, targets, dynamic_mask, views_per_call,
                           buffers, atlas_grad, done, s);
   cudaEventDestroy(fork);

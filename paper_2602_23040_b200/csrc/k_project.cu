@@ -13,7 +13,7 @@ namespace puv {
 
 template <int DEG>
 #ifndef PUV_PROJ_MINB
-#define PUV_PROJ_MINB 1
+#define PUV_PROJ_MINB 3
 #endif
 __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ, int N,
                                                  const __grid_constant__ CamBatch cb, Views v, int gx, int gy) {

@@ -132,7 +132,9 @@ __device__ __forceinline__ bool block_may_hit(float mx, float my, float ha, floa
   if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return tg <= 0.f;
   const float dxm = fmaxf(fabsf(dxl), fabsf(dxh)), dym = fmaxf(fabsf(dyl), fabsf(dyh));
   const float margin = 1e-3f * (fabsf(ha) * dxm * dxm + fabsf(nb) * dxm * dym + fabsf(hc) * dym * dym) + 1e-4f;
-  const float ihc = -0.5f / hc, iha = -0.5f / ha;   // vertex of q along y (resp. x): d* = -nb e / (2 hc)
+  // vertex of q along y (resp. x): d* = -nb e / (2 hc); a fast reciprocal is enough: a vertex off by
+  // delta ~ 1e-7 |d*| only lowers that edge's value by |hc| delta^2 < 1e-9, far inside the margin
+  const float ihc = __fdividef(-0.5f, hc), iha = __fdividef(-0.5f, ha);
   float best = -INFINITY;
   {
     const float dy = fminf(fmaxf(nb * dxl * ihc, dyl), dyh);

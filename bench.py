@@ -229,6 +229,17 @@ def roofline(stage, per_view, D, views_in_stage, stage_ms, calls, peaks, nsm, fp
                                     f"+ {K5_PER_COMPOSITED} per composited pair",
                       "raster_bwd": f"SURVEY §8(d): {K6_PER_EXAMINED} per examined + {K6_PER_COMPOSITED} per "
                                     "composited pair"}[stage]}
+        if stage in ("raster_fwd", "raster_bwd"):
+            # this design's own algorithmic work (DESIGN.md §6/§14): the fp32 contract per composited pair
+            # (exp_c, cap, transmittance, termination: ~20 in K5; K6 replays decisions from K5's bits) plus
+            # its fp64 value path at two fp32 lanes per fp64 lane-op
+            e, p_ = per_view["examined"], per_view["composited"]
+            own = ((8 * e + 20 * p_ + 2 * 18 * p_) if stage == "raster_fwd" else (2 * 32 * p_)) \
+                * views_in_stage / max(calls, 1)
+            r["design_work"] = {"achieved": own / avg_launch_s / 1e12, "peak": peak,
+                                "frac": own / avg_launch_s / 1e12 / peak, "unit": "T FP32-equivalent lane-instr/s",
+                                "work": ("8 fp32 per examined pair + (20 fp32 contract + 2 x 18 fp64) per composited pair"
+                                         if stage == "raster_fwd" else "2 x 32 fp64 per composited pair")}
         if fp64_secondary:
             # the build's own value path: fp64 lane-ops per composited pair vs 64 FP64 lanes/SM
             n64 = {"raster_fwd": 18, "raster_bwd": 32}[stage] * per_view["composited"] * views_in_stage / max(calls, 1)

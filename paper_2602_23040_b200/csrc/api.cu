@@ -460,6 +460,9 @@ struct L2Hook {
   float* dL;
   double* loss;
   cudaEvent_t targets_ready;   // nullable: the per-view losses wait for it (e.g. an H2D copy of targets)
+  bool backward;               // also the per-view composite backward (the fused step); else losses only
+  void* zero_ptr;              // nullable: zeroed on the second stream first (K6's moment slots)
+  size_t zero_bytes;
 };
 
 // Project, bin and composite all views of a call (rows a1-a5); with `hook`, also rows a6-a7 per
@@ -486,6 +489,8 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
   for (int i = 0; i < p.nscratch; ++i) cudaStreamWaitEvent(ss.s[i], ss.fork, 0);
   if (hook) {
     cudaStreamWaitEvent(ss.s2, ss.fork, 0);
+    // HBM-bound zeroing beside the compute-bound compositing instead of in front of the backward
+    if (hook->zero_bytes) cudaMemsetAsync(hook->zero_ptr, 0, hook->zero_bytes, ss.s2);
     if (hook->targets_ready) cudaStreamWaitEvent(ss.s2, hook->targets_ready, 0);
   }
   // Views are composited in groups of kFwdGroup consecutive views per launch (grid.y), each
@@ -513,8 +518,10 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
         const size_t off = (size_t)g0 * 3 * p.HW, n = (size_t)(v + 1 - g0) * 3 * p.HW;
         { StageScope sc(PUV_STAGE_LOSS, ss.s2);
           launch_l2_loss((int64_t)n, images + off, hook->targets + off, hook->dL + off, hook->loss, ss.s2, true); }
-        { StageScope sc(PUV_STAGE_RASTER_BWD, ss.s2);
-          launch_raster_bwd(p, c.views, (const uint32_t*)arena, hook->dL + off, g0, v + 1 - g0, ss.s2); }
+        if (hook->backward) {
+          StageScope sc(PUV_STAGE_RASTER_BWD, ss.s2);
+          launch_raster_bwd(p, c.views, (const uint32_t*)arena, hook->dL + off, g0, v + 1 - g0, ss.s2);
+        }
       }
     }
   }
@@ -701,7 +708,7 @@ puv_status puv_render_l2_step(const puv_layout* layout, const float* const* atla
   cudaStream_t s = (cudaStream_t)stream;
   cudaMemsetAsync(loss, 0, sizeof(double), s);
   cudaMemsetAsync(c.views.grad2d, 0, (size_t)72 * n_views * c.plan.N, s);   // K6's moment slots
-  const L2Hook hook{targets, dL_dimages, loss, (cudaEvent_t)targets_ready};
+  const L2Hook hook{targets, dL_dimages, loss, (cudaEvent_t)targets_ready, true, nullptr, 0};
   render_pipeline(c, atlas_occ, n_views, cams, bg, images, state, arena, arena_bytes, s, &hook);
   project_backward(c, atlas_occ, n_views, cams, dynamic_mask, G, s);
   return cuda_check("puv_render_l2_step");
@@ -738,12 +745,12 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
     Common cc = c;
     cc.plan = make_plan(*layout, n, c.W, c.H);   // offsets of an n-view call (fits: n <= chunk)
     cc.views = views_of(cc.plan, b->state);
-    render_pipeline(cc, atlas_occ, n, cams + v0, bg, b->images, b->state, b->arena, b->arena_bytes, s, nullptr);
+    // each view's loss gradient on the second stream as soon as it is composited, and the zeroing
+    // of K6's moment slots there too: both overlap the compositing of later views
+    const L2Hook hook{targets + (size_t)v0 * HW3, b->dL_dimages, b->loss, v0 == 0 ? targets_ready : nullptr, false,
+                      cc.views.grad2d, (size_t)72 * n * cc.plan.N};
+    render_pipeline(cc, atlas_occ, n, cams + v0, bg, b->images, b->state, b->arena, b->arena_bytes, s, &hook);
     launch_overflow_acc(b->state, b->overflow, b->arena_need, s);
-    if (targets_ready && v0 == 0) cudaStreamWaitEvent(s, targets_ready, 0);
-    { StageScope sc(PUV_STAGE_LOSS, s);
-      launch_l2_loss((int64_t)(n * HW3), b->images, targets + (size_t)v0 * HW3, b->dL_dimages, b->loss, s, true); }
-    cudaMemsetAsync(cc.views.grad2d, 0, (size_t)72 * n * cc.plan.N, s);
     { StageScope sc(PUV_STAGE_RASTER_BWD, s);
       launch_raster_bwd(cc.plan, cc.views, (const uint32_t*)b->arena, b->dL_dimages, 0, n, s); }
     project_backward(cc, atlas_occ, n, cams + v0, dynamic_mask, G, s);

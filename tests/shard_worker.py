@@ -39,6 +39,42 @@ def scene_views(cfg, views):
     return sc
 
 
+def frame_setup(dev):
+    """C4 frames {0, 29} x views {0, 27, 54} (FrameStep): layout, per-frame plane tables, labels, targets."""
+    from synth.scenes import frame_positions
+    sc = make_scene(4)
+    lv = sc.levels[0]
+    layout = puv.layout_for_levels([(lv.rows, lv.cols)], 3)
+    base = torch.from_numpy(lv.planes).to(dev)
+    occ = torch.from_numpy(lv.occ).to(dev)
+    labels = torch.from_numpy(lv.labels).to(dev)
+    frames, views = [0, 29], [0, 27, 54]
+    pos = [torch.from_numpy(frame_positions(sc, f)).to(dev) for f in frames]
+    tables = [[p[0], p[1], p[2]] + [base[d] for d in range(3, layout.planes)] for p in pos]
+    return sc, layout, occ, labels, frames, views, tables, pos
+
+
+def frame_targets(sc, frames, views, idx, dev):
+    return torch.from_numpy(np.stack([sc.target(views[v], frame=frames[f]) for f, v in idx])).to(dev)
+
+
+def main_frames(outdir, rank, world, dev):
+    from paper_2602_23040_b200.shard import FrameStep
+    sc, layout, occ, labels, frames, views, tables, pos = frame_setup(dev)
+    fs = FrameStep(layout, [sc.cameras[v] for v in views], len(frames), rank, world, dev, dynamic=labels)
+    tg = frame_targets(sc, frames, views, fs.local_targets_index(), dev)
+    grads = torch.empty((2, layout.planes, layout.atlas_h, layout.atlas_w), dtype=torch.float32, device=dev)
+    fs.world = 1                                   # the local gradients, before the exchange
+    fs.step(tables, occ, tg, grads, mask=labels)
+    torch.cuda.synchronize()
+    local = grads.cpu().numpy()
+    fs.world = world
+    loss = fs.step(tables, occ, tg, grads, mask=labels)
+    torch.cuda.synchronize()
+    np.savez(os.path.join(outdir, f"frames_rank{rank}.npz"), local=local, grad=grads.cpu().numpy(),
+             loss=np.array([loss.item()]), pairs=np.array(fs.pairs))
+
+
 def main():
     cfg = int(sys.argv[1])
     views = None if sys.argv[2] == "all" else [int(x) for x in sys.argv[2].split(",")]
@@ -47,6 +83,11 @@ def main():
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    if cfg == 4:
+        main_frames(outdir, rank, world, dev)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     sc = scene_views(cfg, views)
     layout = puv.layout_for_levels([(lv.rows, lv.cols) for lv in sc.levels], sc.sh_degree)
     atlas, occ = puv.pack_atlas(layout, [torch.from_numpy(lv.planes).to(dev) for lv in sc.levels],

@@ -22,7 +22,7 @@ from paper_2602_23040_b200 import puv
 from paper_2602_23040_b200.shard import ShardedStep, local_views
 from synth.scenes import make_scene
 from tests.gpu_common import GRAD_ATOL, GRAD_RTOL, oracle_scene
-from tests.shard_worker import digests, scene_views
+from tests.shard_worker import digests, frame_setup, frame_targets, scene_views
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -161,3 +161,45 @@ def test_view_chunks_equal_one_call_c2():
     assert ov and need > 4096
     Ls = small.step(atlas, occ, tg, gc).item()
     assert not small.overflowed() and abs(Ls - L1) <= 1e-12 * L1
+
+
+def test_two_ranks_frame_step_c4(tmp_path):
+    """C4's FrameStep at world size 2 on the one GPU: the 6 (frame, view) pairs of frames {0, 29} x
+    views {0, 27, 54} dealt round-robin, each rank's per-frame gradients frozen on static texels,
+    then the compacted exchange over the dynamic texels: every rank ends with the fp32 sum of the
+    two ranks' local gradients (up to atomic-order noise), = the world-1 FrameStep up to that
+    summation order, static texels exactly zero, and the loss = the world-1 loss."""
+    from paper_2602_23040_b200.shard import FrameStep, local_pairs
+    dev = torch.device("cuda")
+    sc, layout, occ, labels, frames, views, tables, pos = frame_setup(dev)
+    fs = FrameStep(layout, [sc.cameras[v] for v in views], len(frames), 0, 1, dev, dynamic=labels)
+    tg = frame_targets(sc, frames, views, fs.local_targets_index(), dev)
+    g1 = torch.empty((2, layout.planes, layout.atlas_h, layout.atlas_w), dtype=torch.float32, device=dev)
+    L1 = fs.step(tables, occ, tg, g1, mask=labels).item()
+    g1 = g1.cpu().numpy().astype(np.float64)
+    del fs, tg
+    torch.cuda.empty_cache()
+    port = _port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   LOCAL_RANK="0")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "shard_worker.py"), "4", "all",
+                                       str(tmp_path)], env=env, cwd=ROOT, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT))
+    for p in procs:
+        out, _ = p.communicate(timeout=900)
+        assert p.returncode == 0, out.decode()[-3000:]
+    res = [np.load(tmp_path / f"frames_rank{r}.npz") for r in range(2)]
+    for r in range(2):
+        assert [tuple(x) for x in res[r]["pairs"]] == local_pairs(2, 3, r, 2)
+    assert np.array_equal(res[0]["grad"], res[1]["grad"])
+    g = res[0]["grad"].astype(np.float64)
+    l0, l1 = res[0]["local"].astype(np.float64), res[1]["local"].astype(np.float64)
+    part = np.abs(l0) + np.abs(l1)
+    s32 = (res[0]["local"] + res[1]["local"]).astype(np.float64)
+    assert np.all(np.abs(g - s32) <= 2 * U32 * part + 1e-30)
+    assert np.all(np.abs(g - g1) <= 4 * U32 * (part + np.abs(g1)) + 1e-30)
+    static = labels.cpu().numpy() == 0
+    assert np.all(g[:, :, static] == 0) and np.abs(g).max() > 0
+    assert abs(res[0]["loss"][0] - L1) <= 1e-12 * L1 and res[0]["loss"][0] == res[1]["loss"][0]

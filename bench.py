@@ -510,7 +510,7 @@ def main():
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
                 "hbm_stages": hbm_stages, "cpu_baseline": cpu,
                 "stage_ms_per_step": {k2: round(v, 4) for k2, v in stage_ms.items() if v > 0},
-                "overlapped_stages": ["depth_sort", "bin"],
+                "overlapped_stages": ["depth_sort", "bin", "loss"],
                 "stage_ms_per_view_serialised": serial,
                 "counts_per_view": c_tot, "overflow": overflow, "loss": loss_value}
         print(json.dumps(line), flush=True)

@@ -18,7 +18,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 python tools/launch_summary.py $O/${TAG}_launches.csv > $O/${TAG}_launches_summary.txt 2>&1
 REPS=""
 for k in k_raster_fwd k_raster_bwd k_project k_project_bwd k_seg_walk k_tile_scatter; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o /tmp/${TAG}_$k \
+  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:$k -c 1 -o /tmp/${TAG}_$k \
     python bench.py --steps 1 --warmup 1 --views 8 --no-e2e --no-cpu-baseline --no-serial >> $O/${TAG}_ncu.log 2>&1
   python tools/ncu_summary.py /tmp/${TAG}_$k.ncu-rep > $O/${TAG}_ncu_${k}_detail.txt 2>&1
 done

@@ -720,7 +720,7 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
                                      const uint8_t* atlas_occ, int32_t n_views, const puv_camera* cams,
                                      const puv_render_opts* opts, const float* targets, const uint8_t* dynamic_mask,
                                      int32_t views_per_call, const puv_step_buffers* b, float* const* atlas_grad,
-                                     cudaEvent_t targets_ready, cudaStream_t s) {
+                                     cudaEvent_t targets_ready, cudaStream_t s, bool validate_only = false) {
   if (!b) return fail(PUV_E_INVALID_ARGUMENT, "buffers is NULL");
   if (!targets || !b->images || !b->dL_dimages || !b->loss || !b->overflow || !b->arena_need)
     return fail(PUV_E_INVALID_ARGUMENT, "NULL targets / images / dL_dimages / loss / overflow / arena_need");
@@ -733,6 +733,7 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
   if (st) return st;
   GradTab G;
   if ((st = grad_table(layout, atlas_grad, G))) return st;
+  if (validate_only) return PUV_OK;
   const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
   const size_t NA = (size_t)layout->atlas_w * layout->atlas_h, HW3 = (size_t)3 * c.W * c.H;
   for (int d = 0; d < layout->planes; ++d)
@@ -786,6 +787,10 @@ puv_status puv_train_step_host(const puv_layout* layout, const float* const* atl
   puv_status st = check_cameras(n_views, cams, W, H);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  // every argument is checked before anything (the uploads included) is enqueued
+  st = train_step_enqueue(layout, atlas_planes, atlas_occ, n_views, cams, opts, targets, dynamic_mask, views_per_call,
+                          buffers, atlas_grad, nullptr, s, true);
+  if (st) return st;
   StreamSet& ss = stream_set(1);
   // this call's own events (recorded once, destroyed after use: resources are released when
   // the recorded work completes), so concurrent calls never share them

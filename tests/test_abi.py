@@ -141,3 +141,48 @@ def test_rho_layout_validation():
     rc = puv.lib().puv_render_views(C.byref(lay), tab, None, 2, cams, C.byref(o), C.c_void_p(1), C.c_void_p(1), sb,
                                     C.c_void_p(1), 16, None)
     assert rc == -1 and "plane 16" in puv.last_error()
+
+
+def test_train_step_argument_validation_without_gpu():
+    """puv_train_step / puv_train_step_host reject bad arguments before enqueueing anything (the
+    uploads of the host-buffer call included): no GPU is touched here."""
+    lay = puv.layout_for_levels([(16, 16)], 0)
+    cams = _cams(3)
+    L = puv.lib()
+    o = puv.opts()
+    sb, _ = puv.query_sizes(lay, puv.cameras([look_at((3, 0, 1), (0, 0, 0), 64, 48, 60.0)] * 2), o)
+    planes = (C.c_void_p * 14)(*([1] * 14))
+    grads = (C.c_void_p * 14)(*([1] * 14))
+
+    def bufs(state_bytes=sb, flags=1):
+        b = puv.StepBuffers()
+        b.images = b.dL_dimages = b.loss = b.state = b.arena = 1
+        b.overflow = b.arena_need = flags
+        b.state_bytes, b.arena_bytes = state_bytes, 16
+        return b
+
+    # views_per_call 2 over 3 views: the state is sized for a 2-view chunk -> accepted by validation;
+    # a 1-view state is too small
+    rc = L.puv_train_step(C.byref(lay), planes, None, 3, cams, C.byref(o), C.c_void_p(1), None, 2,
+                          C.byref(bufs(16)), grads, None)
+    assert rc == -6
+    rc = L.puv_train_step(C.byref(lay), planes, None, 3, cams, C.byref(o), C.c_void_p(1), None, 2,
+                          C.byref(bufs(flags=0)), grads, None)
+    assert rc == -1 and "overflow" in puv.last_error()
+    bad_grads = (C.c_void_p * 14)(*([1] * 13 + [0]))
+    rc = L.puv_train_step(C.byref(lay), planes, None, 3, cams, C.byref(o), C.c_void_p(1), None, 2,
+                          C.byref(bufs()), bad_grads, None)
+    assert rc == -1 and "grad plane 13" in puv.last_error()
+    bad = _cams(3)
+    bad[2].fx = -1.0    # a camera outside the first chunk is checked too
+    rc = L.puv_train_step(C.byref(lay), planes, None, 3, bad, C.byref(o), C.c_void_p(1), None, 2,
+                          C.byref(bufs()), grads, None)
+    assert rc == -5
+    up = (puv.Copy * 1)(puv.Copy(1, 1, 64))
+    rc = L.puv_train_step_host(C.byref(lay), planes, None, 3, cams, C.byref(o), up, 1, C.c_void_p(1), C.c_void_p(1),
+                               None, 2, C.byref(bufs(16)), grads, None, 0, None)
+    assert rc == -6
+    up0 = (puv.Copy * 1)(puv.Copy(0, 1, 64))
+    rc = L.puv_train_step_host(C.byref(lay), planes, None, 3, cams, C.byref(o), up0, 1, C.c_void_p(1), C.c_void_p(1),
+                               None, 2, C.byref(bufs()), grads, None, 0, None)
+    assert rc == -1 and "upload 0" in puv.last_error()

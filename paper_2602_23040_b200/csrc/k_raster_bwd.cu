@@ -42,6 +42,9 @@ namespace puv {
 constexpr int kBwdPPT = PUV_BWD_PPT;                       // pixels per thread (one column, rows r + 4k)
 constexpr int kBwdThreads = kTile * kTile / kBwdPPT;        // 128 (PPT 2) or 64 (PPT 4)
 constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4-bank skew per row
+#ifndef PUV_BWD_EXPSEL
+#define PUV_BWD_EXPSEL 1
+#endif
 #ifndef PUV_BWD_CULL
 #define PUV_BWD_CULL 1
 #endif
@@ -283,8 +286,16 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
 #pragma unroll
         for (int k = 0; k < kBwdPPT; ++k) {
           const double dy = d0.y - dj[k];
+#if PUV_BWD_EXPSEL
+          // an inactive pixel gets G = e^-700 (~1e-304): its alpha, moments and colour terms vanish
+          // below any nonzero fp64 sum, so the two result selects become one argument select
+          const double pw = power64(d2.x, hadxx, nbdx, dy);
+          const double G = exp64(act[k] ? pw : -700.0, sExp);
+          double a = o * G;
+#else
           const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
           double a = act[k] ? o * G : 0.0;
+#endif
           if (kCap) a = cap[k] ? 0.99 : a;
           const double aT = a * T[k];
           const double cd = fma(dC[k][0], d3.x, fma(dC[k][1], d3.y, dC[k][2] * cb));
@@ -293,7 +304,11 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
           gv[6] = fma(aT, dC[k][0], gv[6]);
           gv[7] = fma(aT, dC[k][1], gv[7]);
           gv[8] = fma(aT, dC[k][2], gv[8]);
+#if PUV_BWD_EXPSEL
+          double GdL = G * dLda;
+#else
           double GdL = act[k] ? G * dLda : 0.0;
+#endif
           if (kCap) GdL = cap[k] ? 0.0 : GdL;   // capped: no gradient through alpha
           gv[5] += GdL;
           sdy = fma(GdL, dy, sdy);

@@ -324,7 +324,10 @@ puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, 
 puv_status puv_overflow_accumulate(const void* state, uint32_t* flag, uint64_t* needed_arena_bytes, void* stream);
 
 /* Per-view debug/parity view of the state (synchronises `stream`).  Host out.
- * Device pointers inside point into state/arena and stay valid until the next call. */
+ * Device pointers inside point into state/arena and stay valid until the next call.  The render
+ * consumes each tile's entries straight from the level-1 super-tile lists (the rect test applied
+ * while K5/K6 stage them), so this call first materialises the view's per-tile lists (level 2 of
+ * the tile pass, into the arena space the render reserved for them): state and arena are written. */
 typedef struct {
   uint32_t n_visible;            /* Gaussians surviving culling in this view */
   uint32_t ntiles, tiles_x, tiles_y;
@@ -343,8 +346,8 @@ typedef struct {
   uint64_t n_composited;         /* pairs composited in the forward */
 } puv_view_debug;
 
-puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, const void* state,
-                          size_t state_bytes, const void* arena, int32_t view, void* stream, puv_view_debug* out);
+puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, void* state,
+                          size_t state_bytes, void* arena, int32_t view, void* stream, puv_view_debug* out);
 
 /* Stage profiling.  When enabled, every library call records a CUDA event pair
  * around each stage on the call's stream (asynchronous, no host sync).

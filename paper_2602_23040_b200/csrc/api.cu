@@ -232,6 +232,11 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   p.ncontrib = take(4 * V * p.HW);
   p.cfull = take(24 * V * p.HW);
   p.dmask = take(32 * V * (size_t)p.ntiles * (size_t)(kMaskCap > 0 ? kMaskCap : 1));
+  p.sgx = (p.gx + kSup - 1) / kSup;
+  p.nst = p.sgx * ((p.gy + kSup - 1) / kSup);
+  p.sst = take(4 * V * (size_t)(p.nst + 1));
+  p.sen = take(4 * V * (size_t)(p.nst + 1));
+  p.l1hdr = take(sizeof(ViewHdr) * V);
   p.sort_blocks = (N + 2047) / 2048;
   // binning scratch: one block per binning stream; offsets below are relative to a block
   size_t soff = 0;
@@ -268,6 +273,11 @@ Views views_of(const Plan& p, void* state) {
   v.ncontrib = (uint32_t*)(s + p.ncontrib);
   v.cfull = (double*)(s + p.cfull);
   v.dmask = (uint32_t*)(s + p.dmask);
+  v.sst = (uint32_t*)(s + p.sst);
+  v.sen = (uint32_t*)(s + p.sen);
+  v.l1 = (ViewHdr*)(s + p.l1hdr);
+  v.sgx = p.sgx;
+  v.nst = p.nst;
   v.hdr = (ViewHdr*)(s + p.view_hdr);
   v.call = (CallHdr*)(s + p.call_hdr);
   return v;
@@ -501,7 +511,7 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
     cudaStream_t bs = serial ? s : ss.s[i];
     void* scratch = (char*)state + p.scratch0 + (size_t)i * p.scratch_stride;
     { StageScope sc(PUV_STAGE_DEPTH_SORT, bs); launch_depth_sort(p, c.views, scratch, v, bs); }
-    { StageScope sc(PUV_STAGE_BIN, bs); launch_bin(p, c.views, scratch, (uint32_t*)arena, v, bs); }
+    { StageScope sc(PUV_STAGE_BIN, bs); launch_bin(p, c.views, scratch, (uint32_t*)arena, v, bs, !kDirect); }
     cudaEvent_t done = ss.view_event(v);
     cudaEventRecord(done, bs);
     cudaStreamWaitEvent(s, done, 0);
@@ -839,8 +849,8 @@ puv_status puv_overflow_accumulate(const void* state, uint32_t* flag, uint64_t* 
   return cuda_check("puv_overflow_accumulate");
 }
 
-puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, const void* state,
-                          size_t state_bytes, const void* arena, int32_t view, void* stream, puv_view_debug* out) {
+puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_camera* cams, void* state,
+                          size_t state_bytes, void* arena, int32_t view, void* stream, puv_view_debug* out) {
   puv_status st = check_layout(layout);
   if (st) return st;
   int W, H;
@@ -849,12 +859,19 @@ puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_c
   if (!state || !out || view < 0 || view >= n_views) return fail(PUV_E_INVALID_ARGUMENT, "bad debug arguments");
   const Plan p = make_plan(*layout, n_views, W, H);
   if (state_bytes < p.total) return fail(PUV_E_WORKSPACE_TOO_SMALL, "state too small");
-  const Views v = views_of(p, (void*)state);
+  const Views v = views_of(p, state);
   ViewHdr h;
   cudaStream_t s = (cudaStream_t)stream;
   cudaMemcpyAsync(&h, v.hdr + view, sizeof h, cudaMemcpyDeviceToHost, s);
   const cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return fail(PUV_E_CUDA, "puv_debug_view: %s", cudaGetErrorString(e));
+  if (kDirect && !h.overflow) {
+    // the render consumed the level-1 super-tile lists directly; materialise this view's per-tile
+    // lists (level 2 of the tile pass, with binning scratch block 0) for the parity / debug view
+    launch_bin_level2(p, v, (char*)state + p.scratch0, (uint32_t*)arena, view, s);
+    const cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e2 != cudaSuccess) return fail(PUV_E_CUDA, "puv_debug_view: %s", cudaGetErrorString(e2));
+  }
   out->n_visible = h.n_vis;
   out->ntiles = p.ntiles;
   out->tiles_x = p.gx;

@@ -34,6 +34,15 @@ constexpr int kMaskCap = PUV_DMASK ? PUV_DMASK_CAP : 0;
 #define PUV_FWD_GROUP 1
 #endif
 constexpr int kFwdGroup = PUV_FWD_GROUP;  // consecutive views per forward-composite launch
+constexpr int kSup = 4;                   // tiles per super-tile side (level 1 of the tile pass)
+constexpr int kSupT = kSup * kSup;        // tiles per super-tile
+#ifndef PUV_DIRECT
+#define PUV_DIRECT 1
+#endif
+// 1: K5/K6 consume each tile's entries straight from its super-tile's rank list (level 1 of the
+// tile pass, in (depth, gid) order) with the rect test of level 2 applied as they stage a batch,
+// so level 2 (materialising the per-tile lists) runs only for the parity / debug view.
+constexpr bool kDirect = PUV_DIRECT != 0;
 constexpr uint32_t kInvisible = 0xFFFFFFFFu;
 
 struct PlaneTab { const float* p[kMaxPlanes]; };
@@ -83,6 +92,8 @@ struct Plan {
   size_t call_hdr, view_hdr;
   // per view arrays, each [n_views][...]
   size_t depth, rect, rec, rec64, grad2d, sorted, tstart, tend, tfinal, ncontrib, cfull, dmask;
+  size_t sst, sen, l1hdr;  // per view: super-tile ranges into the level-1 rank list, its header
+  int sgx, nst;            // super-tiles per row, super-tiles
   // scratch shared by all views (reused in stream order)
   // (offsets relative to one scratch block; block i starts at scratch0 + i * scratch_stride)
   size_t sk0, sv0, sk1, sv1, hist, koff, bsum, cnt, bstart, bin2;
@@ -108,6 +119,10 @@ struct Views {
   uint32_t* ncontrib;// [V][HW]
   double* cfull;     // [V][HW][3]  fp64 full colour sum c a T + T_final bg (forward -> backward)
   uint32_t* dmask;   // [V][ntiles][kMaskCap][8]  composited-pixel bitmask per (tile, entry) (K5 -> K6)
+  uint32_t* sst;     // [V][nst + 1]  super-tile range start in the view's level-1 rank list
+  uint32_t* sen;     // [V][nst + 1]  ... end
+  ViewHdr* l1;       // [V]  level-1 header (list_base of the rank lists, K1, overflow)
+  int sgx, nst;      // super-tiles per row, super-tiles
   ViewHdr* hdr;      // [V]
   CallHdr* call;
 };
@@ -135,7 +150,8 @@ size_t bin_scratch_bytes(size_t N, int ntiles);
 void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,
                     cudaStream_t s);
 void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cudaStream_t s);
-void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
+void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s, bool level2);
+void launch_bin_level2(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
 void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* images, int view0, int n_views,
                        const float bg[3], cudaStream_t s);
 void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int view0,

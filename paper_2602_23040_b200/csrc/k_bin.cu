@@ -475,8 +475,6 @@ __global__ void __launch_bounds__(kBinThreads) k_tile_scatter(const ViewHdr* hdr
 // tile list comes out in rank = (depth_bits, gid) order with one coalesced run of writes per
 // (32 ranks, tile).
 
-constexpr int kSup = 4;                    // tiles per super-tile side
-constexpr int kSupT = kSup * kSup;         // tiles per super-tile
 #ifndef PUV_SEG_MIN
 #define PUV_SEG_MIN 512
 #endif
@@ -689,7 +687,58 @@ size_t bin_scratch_bytes(size_t N, int ntiles) {
          3 * align_up(4 * ((size_t)ntiles + 1)) + align_up(4 * ms) + align_up(4 * ms * kSupT);
 }
 
-void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s) {
+// Level-2 scratch carved from a binning scratch block (at p.bin2).
+struct Bin2 {
+  uint4* rk;
+  uint2* srect;
+  unsigned long long* ktot;
+  L2Info* info;
+  uint32_t *segbase, *segst, *cnt2;
+};
+
+static Bin2 bin2_of(const Plan& p, void* state) {
+  char* b2 = (char*)state + p.bin2;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { char* q = b2 + o; o += align_up(bytes); return q; };
+  Bin2 b;
+  b.rk = (uint4*)take(16 * (size_t)p.N);
+  b.srect = (uint2*)take(8 * (size_t)p.N);
+  b.ktot = (unsigned long long*)take(16);
+  b.info = (L2Info*)take(sizeof(L2Info));
+  b.segbase = (uint32_t*)take(4 * ((size_t)p.ntiles + 1));
+  b.segst = (uint32_t*)take(4 * max_segments(p.ntiles));
+  b.cnt2 = (uint32_t*)take(4 * max_segments(p.ntiles) * kSupT);
+  return b;
+}
+
+// Level 2 (per-tile lists from the super-tile rank lists): on the render path when !kDirect, else on
+// demand for the debug / parity view of one view (the level-1 lists, super-tile ranges and header
+// persist per view; rk is rebuilt here since a later view may have reused the scratch block).
+static void level2(const Plan& p, const Views& v, const Bin2& b, uint32_t* arena, int view, cudaStream_t s) {
+  ViewHdr* hdr = v.hdr + view;
+  const ViewHdr* l1 = v.l1 + view;
+  const uint32_t* sst = v.sst + (size_t)view * (p.nst + 1);
+  const uint32_t* sen = v.sen + (size_t)view * (p.nst + 1);
+  uint32_t* tstart = v.tstart + (size_t)view * p.ntiles;
+  uint32_t* tend = v.tend + (size_t)view * p.ntiles;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  k_seg_plan<<<1, 1024, 0, s>>>(l1, sst, sen, p.nst, b.segbase, b.segst, b.info);
+#ifndef PUV_WALK_CTAS_PER_SM
+#define PUV_WALK_CTAS_PER_SM 8
+#endif
+  const int wblocks = PUV_WALK_CTAS_PER_SM * nsm;   // 8 warps per block, grid-stride over segments
+  k_seg_walk<1><<<wblocks, 256, 0, s>>>(hdr, l1, b.info, b.segbase, b.segst, sst, sen, arena, b.rk, p.sgx, p.gx,
+                                        p.gy, b.cnt2, nullptr, nullptr);
+  k_seg_offsets<<<(p.nst + 7) / 8, 256, 0, s>>>(l1, b.segbase, p.sgx, p.nst, p.gx, p.gy, b.cnt2, tend /* totals */);
+  k_tile_ranges<<<1, 1024, 0, s>>>(tend, p.ntiles, tstart, tend);
+  k_seg_walk<2><<<wblocks, 256, 0, s>>>(hdr, l1, b.info, b.segbase, b.segst, sst, sen, arena, b.rk, p.sgx, p.gx,
+                                        p.gy, b.cnt2, tstart, arena);
+  count_launches(5);
+}
+
+void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s, bool with_level2) {
   char* st = (char*)state;
   const uint32_t* sorted = v.sorted + (size_t)view * p.N;
   const uint2* rect = v.rect + (size_t)view * p.N;
@@ -698,33 +747,21 @@ void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int
   uint32_t* koff1 = (uint32_t*)(st + p.koff);
   uint32_t* cnt = (uint32_t*)(st + p.cnt);
   uint32_t* bstart = (uint32_t*)(st + p.bstart);
-  uint32_t* tstart = v.tstart + (size_t)view * p.ntiles;
-  uint32_t* tend = v.tend + (size_t)view * p.ntiles;
-  // level-2 scratch (carved from the block at p.bin2)
-  char* b2 = st + p.bin2;
-  size_t o = 0;
-  auto take = [&](size_t bytes) { char* q = b2 + o; o += align_up(bytes); return q; };
-  const int sgx = (p.gx + kSup - 1) / kSup, sgy = (p.gy + kSup - 1) / kSup, nst = sgx * sgy;
-  uint4* rk = (uint4*)take(16 * (size_t)p.N);
-  uint2* srect = (uint2*)take(8 * (size_t)p.N);
-  ViewHdr* l1 = (ViewHdr*)take(sizeof(ViewHdr));
-  unsigned long long* ktot = (unsigned long long*)take(16);
-  L2Info* info = (L2Info*)take(sizeof(L2Info));
-  uint32_t* sst = (uint32_t*)take(4 * ((size_t)p.ntiles + 1));
-  uint32_t* sen = (uint32_t*)take(4 * ((size_t)p.ntiles + 1));
-  uint32_t* segbase = (uint32_t*)take(4 * ((size_t)p.ntiles + 1));
-  uint32_t* segst = (uint32_t*)take(4 * max_segments(p.ntiles));
-  uint32_t* cnt2 = (uint32_t*)take(4 * max_segments(p.ntiles) * kSupT);
+  const Bin2 b = bin2_of(p, state);
+  ViewHdr* l1 = v.l1 + view;
+  uint32_t* sst = v.sst + (size_t)view * (p.nst + 1);
+  uint32_t* sen = v.sen + (size_t)view * (p.nst + 1);
+  const int sgx = p.sgx, sgy = (p.gy + kSup - 1) / kSup, nst = p.nst;
   uint64_t* k1tot = &l1->ktotal;
 
-  cudaMemsetAsync(ktot, 0, 16, s);
-  k_bin_prep<<<(p.N + 255) / 256, 256, 0, s>>>(hdr, sorted, rect, rk, srect, ktot);
+  cudaMemsetAsync(b.ktot, 0, 16, s);
+  k_bin_prep<<<(p.N + 255) / 256, 256, 0, s>>>(hdr, sorted, rect, b.rk, b.srect, b.ktot);
   // level-1 key offsets per rank (super-tile keys), K1
   const int nsb = p.N / kScanTile + 1;   // one extra block so koff1[n_vis] (= K1) is always written
-  k_koff_reduce<<<nsb, kScanThreads, 0, s>>>(nullptr, srect, hdr, bsum);
+  k_koff_reduce<<<nsb, kScanThreads, 0, s>>>(nullptr, b.srect, hdr, bsum);
   k_scan_bsum<<<1, 1024, 0, s>>>(bsum, nsb, k1tot);
-  k_koff_write<<<nsb, kScanThreads, 0, s>>>(nullptr, srect, hdr, bsum, koff1);
-  k_view_finalize2<<<1, 1, 0, s>>>(hdr, v.call, ktot, k1tot, l1);
+  k_koff_write<<<nsb, kScanThreads, 0, s>>>(nullptr, b.srect, hdr, bsum, koff1);
+  k_view_finalize2<<<1, 1, 0, s>>>(hdr, v.call, b.ktot, k1tot, l1);
   k_block_starts<<<(kNbMax + 255) / 256, 256, 0, s>>>(l1, koff1, bstart);
 
   int dev = 0, nsm = 148;
@@ -733,25 +770,24 @@ void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int
   // level 1: stable counting sort of super-tile keys (ranks) by super-tile
   const int band_rows = sgx >= kBandTiles ? 1 : (kBandTiles / sgx < sgy ? kBandTiles / sgx : sgy);
   const int nbands = (sgy + band_rows - 1) / band_rows;
-  k_tile_count<<<PUV_BIN_CTAS_PER_SM * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
-                                              cnt);
+  k_tile_count<<<PUV_BIN_CTAS_PER_SM * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, b.srect, bstart, sgx, sgy,
+                                                                 band_rows, nbands, nst, cnt);
   k_col_scan<<<(nst + 31) / 32, 1024, 0, s>>>(l1, cnt, nst, sen /* totals */);
   k_tile_ranges<<<1, 1024, 0, s>>>(sen, nst, sst, sen);
-  k_tile_scatter<<<PUV_BIN_CTAS_PER_SM * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, srect, bstart, sgx, sgy, band_rows, nbands, nst,
-                                                cnt, sst, arena + 0);
-  // level 2: per-tile lists from the super-tile rank lists
-  k_seg_plan<<<1, 1024, 0, s>>>(l1, sst, sen, nst, segbase, segst, info);
-#ifndef PUV_WALK_CTAS_PER_SM
-#define PUV_WALK_CTAS_PER_SM 8
-#endif
-  const int wblocks = PUV_WALK_CTAS_PER_SM * nsm;   // 8 warps per block, grid-stride over segments
-  k_seg_walk<1><<<wblocks, 256, 0, s>>>(hdr, l1, info, segbase, segst, sst, sen, arena, rk, sgx, p.gx, p.gy, cnt2,
-                                        nullptr, nullptr);
-  k_seg_offsets<<<(nst + 7) / 8, 256, 0, s>>>(l1, segbase, sgx, nst, p.gx, p.gy, cnt2, tend /* totals */);
-  k_tile_ranges<<<1, 1024, 0, s>>>(tend, p.ntiles, tstart, tend);
-  k_seg_walk<2><<<wblocks, 256, 0, s>>>(hdr, l1, info, segbase, segst, sst, sen, arena, rk, sgx, p.gx, p.gy, cnt2,
-                                        tstart, arena);
-  count_launches(16);
+  k_tile_scatter<<<PUV_BIN_CTAS_PER_SM * nsm, kBinThreads, 0, s>>>(l1, koff1, nullptr, b.srect, bstart, sgx, sgy,
+                                                                   band_rows, nbands, nst, cnt, sst, arena + 0);
+  count_launches(11);
+  if (with_level2) level2(p, v, b, arena, view, s);
+}
+
+void launch_bin_level2(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s) {
+  const Bin2 b = bin2_of(p, state);
+  // rk (rect + gid per rank) of this view, again
+  cudaMemsetAsync(b.ktot, 0, 16, s);
+  k_bin_prep<<<(p.N + 255) / 256, 256, 0, s>>>(v.hdr + view, v.sorted + (size_t)view * p.N,
+                                               v.rect + (size_t)view * p.N, b.rk, b.srect, b.ktot);
+  count_launches(1);
+  level2(p, v, b, arena, view, s);
 }
 
 }  // namespace puv

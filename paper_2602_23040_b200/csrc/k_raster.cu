@@ -14,6 +14,7 @@
 // carried in fp64: the image is the fp64 colour rounded once, and the pixel's full
 // colour C = sum c_k a_k T_k + T_final bg is kept for the single-pass backward (K6).
 #include "contract.cuh"
+#include "feed.cuh"
 #include "internal.cuh"
 
 namespace puv {
@@ -74,11 +75,30 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
   float* image = images + (size_t)blockIdx.y * 3 * W * H;
   const ViewHdr& hdr = v.hdr[view];
   uint32_t start = 0, end = 0;
+#if PUV_DIRECT
+  // the tile's entries: its super-tile's level-1 rank range, filtered by rect (feed.cuh)
+  __shared__ uint32_t sGid[2 * kFwdBatch], sFeedCnt[kRasterThreads / 32 + 1];
+  TileFeed<kRasterThreads, kFwdBatch> feed;
+  {
+    const int st = (ty / kSup) * v.sgx + (tx / kSup);
+    const ViewHdr& l1 = v.l1[view];
+    if (!hdr.overflow && !l1.overflow) {
+      start = v.sst[(size_t)view * (v.nst + 1) + st];
+      end = v.sen[(size_t)view * (v.nst + 1) + st];
+    }
+    feed.init(sGid, sFeedCnt, start, end);
+  }
+  const uint32_t* list1 = arena + v.l1[view].list_base;
+  const uint32_t* sorted_v = v.sorted + (size_t)view * N;
+  const uint2* rect_v = v.rect + (size_t)view * N;
+  uint32_t ebase = 0;   // tile-list entries before the current batch
+#else
   if (!hdr.overflow) {
     start = v.tstart[(size_t)view * ntiles + tile];
     end = v.tend[(size_t)view * ntiles + tile];
   }
   const uint32_t* list = arena + hdr.list_base;
+#endif
   const float4* rec = v.rec + (size_t)view * N * 2;
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   const float fi = (float)px;
@@ -107,6 +127,26 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
                               : nullptr;
 #pragma unroll
   for (int k = 0; k < kFwdPPT; ++k) exam[k] = 0;
+#if PUV_DIRECT
+  for (;;) {
+    if (__syncthreads_count(all_of(done)) == kRasterThreads) break;
+    const int nb = feed.next(list1, sorted_v, rect_v, tx, ty);
+    if (nb == 0) break;
+#pragma unroll
+    for (int i = threadIdx.x; i < kFwdBatch; i += kRasterThreads) {
+      if (i < nb) {
+        const uint32_t g = sGid[i];
+        PUV_CHECK(g < (uint32_t)N);
+        sA[i] = rec[2 * (size_t)g + 0];
+        sB[i] = rec[2 * (size_t)g + 1];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) sD[k][i] = rec64[5 * (size_t)g + k];
+      }
+    }
+    __syncthreads();
+    const int n = __all_sync(0xffffffffu, all_of(done)) ? 0 : nb;
+    const uint32_t b0 = ebase + start;   // so that b0 + j - start is the entry index below
+#else
   for (uint32_t b0 = start; b0 < end; b0 += kFwdBatch) {
     if (__syncthreads_count(all_of(done)) == kRasterThreads) break;
 #pragma unroll
@@ -123,6 +163,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
     }
     __syncthreads();
     const int n = __all_sync(0xffffffffu, all_of(done)) ? 0 : (int)min((uint32_t)kFwdBatch, end - b0);
+#endif
 #if PUV_FWD_CULL
     // per-warp filter: one box test per staged entry (lanes split the batch), ballots -> the
     // entries whose ellipse can reach this warp's 8x8 block; the walk visits only those (the
@@ -234,10 +275,19 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         break;
       }
     }
+#if PUV_DIRECT
+    ebase += (uint32_t)nb;
+    feed.pop(nb);
+#endif
   }
+#if PUV_DIRECT
+  const uint32_t list_len = ebase;   // the whole list was fed unless every pixel terminated first
+#else
+  const uint32_t list_len = end - start;
+#endif
   uint32_t n_exam = 0;
 #pragma unroll
-  for (int k = 0; k < kFwdPPT; ++k) n_exam += done[k] ? exam[k] : (px < W && py0 + 4 * k < H ? end - start : 0u);
+  for (int k = 0; k < kFwdPPT; ++k) n_exam += done[k] ? exam[k] : (px < W && py0 + 4 * k < H ? list_len : 0u);
   {  // pair statistics (one atomic per warp)
     const uint32_t we = __reduce_add_sync(0xffffffffu, n_exam), wc = __reduce_add_sync(0xffffffffu, n_comp);
     if (lane == 0 && (we | wc)) {

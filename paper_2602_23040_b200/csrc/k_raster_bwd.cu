@@ -24,6 +24,7 @@
 #include <type_traits>
 
 #include "contract.cuh"
+#include "feed.cuh"
 #include "internal.cuh"
 
 namespace puv {
@@ -32,7 +33,7 @@ namespace puv {
 #define PUV_BWD_PPT 4
 #endif
 #ifndef PUV_BWD_MINB
-#define PUV_BWD_MINB 0
+#define PUV_BWD_MINB 8
 #endif
 #if PUV_BWD_MINB > 0
 #define PUV_BWD_BOUNDS __launch_bounds__(kTile * kTile / PUV_BWD_PPT, PUV_BWD_MINB)
@@ -136,8 +137,24 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const ViewHdr& hdr = v.hdr[view];
   if (hdr.overflow) return;
+#if PUV_DIRECT
+  // the tile's entries: its super-tile's level-1 rank range, filtered by rect (feed.cuh)
+  __shared__ uint32_t sGid[2 * kBwdBatch], sFeedCnt[kBwdThreads / 32 + 1];
+  TileFeed<kBwdThreads, kBwdBatch> feed;
+  {
+    const ViewHdr& l1 = v.l1[view];
+    const int st = (ty / kSup) * v.sgx + (tx / kSup);
+    const uint32_t c0 = l1.overflow ? 0u : v.sst[(size_t)view * (v.nst + 1) + st];
+    const uint32_t c1 = l1.overflow ? 0u : v.sen[(size_t)view * (v.nst + 1) + st];
+    feed.init(sGid, sFeedCnt, c0, c1);
+  }
+  const uint32_t* list1 = arena + v.l1[view].list_base;
+  const uint32_t* sorted_v = v.sorted + (size_t)view * N;
+  const uint2* rect_v = v.rect + (size_t)view * N;
+#else
   const uint32_t start = v.tstart[(size_t)view * ntiles + tile];
   const uint32_t* list = arena + hdr.list_base + start;
+#endif
   const float4* rec = v.rec + (size_t)view * N * 2;
   const double2* rec64 = v.rec64 + (size_t)view * N * 5;
   double* g2 = v.grad2d + (size_t)view * N * 9;
@@ -181,6 +198,16 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
 #pragma unroll
   for (int w = 0; w < kBwdThreads / 32; ++w) bmax = max(bmax, smax[w]);
 
+#if PUV_DIRECT
+  for (uint32_t lo = 0; lo < bmax;) {
+    const int nb = feed.next(list1, sorted_v, rect_v, tx, ty);
+    if (nb == 0) break;
+    const int n = (int)min((uint32_t)nb, bmax - lo);
+    for (int i = threadIdx.x; i < n; i += kBwdThreads) {
+      const uint32_t g = sGid[i];
+      PUV_CHECK(g < (uint32_t)N);
+      sG[i] = g;
+#else
   for (uint32_t lo = 0; lo < bmax; lo += kBwdBatch) {
     const int n = (int)min((uint32_t)kBwdBatch, bmax - lo);
     __syncthreads();
@@ -188,6 +215,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       const uint32_t g = list[lo + i];
       PUV_CHECK(g < (uint32_t)N && start + lo + i < hdr.K);
       sG[i] = g;
+#endif
       sA[i] = rec[2 * (size_t)g + 0];
       sB[i] = rec[2 * (size_t)g + 1];
 #pragma unroll
@@ -337,6 +365,10 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       if (lane < 27 && lane % 3 == 0) atomicAdd(g2 + 9 * (size_t)sG[j] + lane / 3, s);
 #endif
     }
+#if PUV_DIRECT
+    lo += (uint32_t)nb;
+    feed.pop(nb);
+#endif
   }
 }
 

@@ -449,10 +449,7 @@ def main():
         last_views = stepper.views
     k0 = (len(last_views) - 1) // st.views_per_call * st.views_per_call
     chunk_cams = puv.cameras([sc.cameras[v] for v in last_views[k0:]])
-    counts = []
-    for i in range(len(chunk_cams)):
-        d = puv.debug_view(layout, chunk_cams, st.state, st.arena, i)
-        counts.append({"n_vis": d.n_visible, "K": d.n_keys, "examined": d.n_examined, "composited": d.n_composited})
+    counts = [puv.view_counts(st.state, i) for i in range(len(chunk_cams))]
     c_tot = {k2: sum(c[k2] for c in counts) / len(counts) for k2 in ("n_vis", "K", "examined", "composited")}
 
     # ---- roofline of the dominant compositing kernel (SURVEY §8(d) basis) ----

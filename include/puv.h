@@ -323,6 +323,12 @@ puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, 
  * flag, needed_arena_bytes: DEVICE pointers (uint32, uint64), caller-initialised. */
 puv_status puv_overflow_accumulate(const void* state, uint32_t* flag, uint64_t* needed_arena_bytes, void* stream);
 
+/* Counters of one view of the last render on `state` (synchronises `stream`), without the tile-list
+ * materialisation of puv_debug_view: counts[0..4] = visible Gaussians, K (keys = sum of tiles
+ * touched), (pixel, entry) pairs examined and composited by the forward, overflow flag.  Host out.
+ * `view` must be < the n_views of that render (not checked: the state carries no view count). */
+puv_status puv_view_counts(const void* state, int32_t view, void* stream, uint64_t* counts);
+
 /* Per-view debug/parity view of the state (synchronises `stream`).  Host out.
  * Device pointers inside point into state/arena and stay valid until the next call.  The render
  * consumes each tile's entries straight from the level-1 super-tile lists (the rect test applied

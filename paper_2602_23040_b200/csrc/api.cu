@@ -890,6 +890,23 @@ puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_c
   return PUV_OK;
 }
 
+puv_status puv_view_counts(const void* state, int32_t view, void* stream, uint64_t* counts) {
+  if (!state || !counts || view < 0) return fail(PUV_E_INVALID_ARGUMENT, "bad view_counts arguments");
+  // the view headers follow the call header at the start of the state (make_plan)
+  const ViewHdr* vh = (const ViewHdr*)((const char*)state + align_up(sizeof(CallHdr))) + view;
+  ViewHdr h;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemcpyAsync(&h, vh, sizeof h, cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(PUV_E_CUDA, "puv_view_counts: %s", cudaGetErrorString(e));
+  counts[0] = h.n_vis;
+  counts[1] = h.overflow ? 0 : h.K;
+  counts[2] = h.examined;
+  counts[3] = h.composited;
+  counts[4] = h.overflow;
+  return PUV_OK;
+}
+
 puv_status puv_debug_contract(int32_t op, const float* in, float* out, int64_t n, void* stream) {
   if ((op != 0 && op != 1) || n < 0 || (n > 0 && (!in || !out))) return fail(PUV_E_INVALID_ARGUMENT, "bad contract args");
   if (n) launch_contract(op, in, out, n, (cudaStream_t)stream);

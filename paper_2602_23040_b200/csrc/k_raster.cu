@@ -37,6 +37,9 @@ constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128 (PPT 2) or 64 (P
 #endif
 constexpr int kFwdBatch = PUV_FWD_BATCH;                 // entries staged per batch
 
+#ifndef PUV_FWD_POPCNT
+#define PUV_FWD_POPCNT 1
+#endif
 #ifndef PUV_FWD_BRANCHFREE
 #define PUV_FWD_BRANCHFREE 0
 #endif
@@ -253,7 +256,9 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         T[k] = Tn;
         last[k] = e + 1;
         comp[k] = true;
+#if !PUV_FWD_POPCNT
         ++n_comp;
+#endif
         // fp64 value of the composited pair
         const double pw = power64(d2.x, hadxx, nbdx, d0.y - dj[k]);
         const double a64 = capped ? 0.99 : d2.y * exp64(pw, sExp);
@@ -266,6 +271,9 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
 #endif
       if (kMaskCap > 0) {
         const uint32_t m0 = __ballot_sync(0xffffffffu, comp[0]), m1 = __ballot_sync(0xffffffffu, comp[1]);
+#if PUV_FWD_POPCNT && !PUV_FWD_BRANCHFREE
+        if (lane == 0) n_comp += __popc(m0) + __popc(m1);   // the warp's composited pairs of this entry
+#endif
         if (lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(m0, m1);
       }
       if (__all_sync(0xffffffffu, all_of(done))) {

@@ -109,6 +109,8 @@ def lib():
         L.puv_train_step_host.argtypes = [P, P, P, S, P, P, P, S, P, P, P, S, P, P, P, S, P]
         L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
         L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
+        L.puv_view_counts.argtypes = [P, S, P, P]
+        L.puv_view_counts.restype = C.c_int32
         L.puv_layout_paper.argtypes = [S, S, S, P]
         L.puv_layout_paper.restype = C.c_int32
         L.puv_ray_planes.argtypes = [P, P, P]
@@ -496,6 +498,14 @@ def check_overflow(state, n_views, stream=None):
     ov, need = C.c_int32(), C.c_uint64()
     _ok(lib().puv_check_overflow(_ptr(state), n_views, _stream(stream), C.byref(ov), C.byref(need)))
     return bool(ov.value), int(need.value)
+
+
+def view_counts(state, view, stream=None) -> dict:
+    """n_visible, K, examined, composited, overflow of one view of the last render (no list materialisation)."""
+    out = (C.c_uint64 * 5)()
+    _ok(lib().puv_view_counts(_ptr(state), int(view), _stream(stream), out))
+    return {"n_vis": int(out[0]), "K": int(out[1]), "examined": int(out[2]), "composited": int(out[3]),
+            "overflow": bool(out[4])}
 
 
 def debug_view(layout, cams, state, arena, view, stream=None) -> ViewDebug:

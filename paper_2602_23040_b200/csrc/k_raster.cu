@@ -38,7 +38,7 @@ constexpr int kRasterThreads = kTile * kTile / kFwdPPT;  // 128 (PPT 2) or 64 (P
 constexpr int kFwdBatch = PUV_FWD_BATCH;                 // entries staged per batch
 
 #ifndef PUV_FWD_POPCNT
-#define PUV_FWD_POPCNT 1
+#define PUV_FWD_POPCNT 0
 #endif
 #ifndef PUV_FWD_BRANCHFREE
 #define PUV_FWD_BRANCHFREE 0

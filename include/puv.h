@@ -326,7 +326,7 @@ puv_status puv_overflow_accumulate(const void* state, uint32_t* flag, uint64_t* 
 /* Counters of one view of the last render on `state` (synchronises `stream`), without the tile-list
  * materialisation of puv_debug_view: counts[0..4] = visible Gaussians, K (keys = sum of tiles
  * touched), (pixel, entry) pairs examined and composited by the forward, overflow flag.  Host out.
- * `view` must be < the n_views of that render (not checked: the state carries no view count). */
+ * `view` must be < the n_views of that render (PUV_E_INVALID_ARGUMENT otherwise). */
 puv_status puv_view_counts(const void* state, int32_t view, void* stream, uint64_t* counts);
 
 /* Per-view debug/parity view of the state (synchronises `stream`).  Host out.

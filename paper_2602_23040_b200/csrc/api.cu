@@ -893,11 +893,17 @@ puv_status puv_debug_view(const puv_layout* layout, int32_t n_views, const puv_c
 puv_status puv_view_counts(const void* state, int32_t view, void* stream, uint64_t* counts) {
   if (!state || !counts || view < 0) return fail(PUV_E_INVALID_ARGUMENT, "bad view_counts arguments");
   // the view headers follow the call header at the start of the state (make_plan)
+  cudaStream_t s = (cudaStream_t)stream;
+  CallHdr ch;
+  cudaMemcpyAsync(&ch, state, sizeof ch, cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(PUV_E_CUDA, "puv_view_counts: %s", cudaGetErrorString(e));
+  if ((uint32_t)view >= ch.n_views)
+    return fail(PUV_E_INVALID_ARGUMENT, "view %d outside the last render's %u views", view, ch.n_views);
   const ViewHdr* vh = (const ViewHdr*)((const char*)state + align_up(sizeof(CallHdr))) + view;
   ViewHdr h;
-  cudaStream_t s = (cudaStream_t)stream;
   cudaMemcpyAsync(&h, vh, sizeof h, cudaMemcpyDeviceToHost, s);
-  const cudaError_t e = cudaStreamSynchronize(s);
+  e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return fail(PUV_E_CUDA, "puv_view_counts: %s", cudaGetErrorString(e));
   counts[0] = h.n_vis;
   counts[1] = h.overflow ? 0 : h.K;

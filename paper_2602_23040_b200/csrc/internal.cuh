@@ -80,7 +80,7 @@ struct CallHdr {
   uint64_t arena_used;    // keys handed out so far (running sum over views)
   uint64_t arena_need;    // keys requested (>= arena_used when overflowing)
   uint32_t overflow_any;
-  uint32_t pad0;
+  uint32_t n_views;       // views of the call (puv_view_counts checks against it)
   uint64_t arena_cap;     // capacity in keys (copied at launch)
   uint64_t pad[4];
 };

@@ -118,7 +118,8 @@ void launch_contract(int op, const float* in, float* out, int64_t n, cudaStream_
   count_launches(1);
 }
 
-__global__ void k_begin_call(CallHdr* call, uint64_t cap) {
+__global__ void k_begin_call(CallHdr* call, uint64_t cap, uint32_t n_views) {
+  call->n_views = n_views;
   call->arena_used = 0;
   call->arena_need = 0;
   call->overflow_any = 0;
@@ -126,7 +127,7 @@ __global__ void k_begin_call(CallHdr* call, uint64_t cap) {
 }
 
 void launch_begin_call(const Plan& p, const Views& v, uint64_t arena_cap, cudaStream_t s) {
-  k_begin_call<<<1, 1, 0, s>>>(v.call, arena_cap);
+  k_begin_call<<<1, 1, 0, s>>>(v.call, arena_cap, (uint32_t)p.n_views);
   count_launches(1);
 }
 

@@ -32,3 +32,17 @@ def test_backward_twice_is_twice(cfg, views):
     # each call rounds its fp64 texel sum once onto the fp32 accumulator: 2 g1 up to that rounding
     # (and the fp64 atomic order of the moments)
     assert np.all(np.abs(b - 2 * a) <= 1e-6 * np.abs(a) + 1e-12), np.abs(b - 2 * a).max()
+
+
+def test_view_counts_match_debug_view_and_check_the_index():
+    sc = make_scene(2)
+    g = gpu_scene(sc, views=[0, 3])
+    g["R"].forward(g["atlas"], g["occ"])
+    for i in range(2):
+        c = puv.view_counts(g["R"].state, i)
+        d = puv.debug_view(g["layout"], g["cams"], g["R"].state, g["R"].arena, i)
+        assert (c["n_vis"], c["K"], c["examined"], c["composited"]) == (d.n_visible, d.n_keys, d.n_examined,
+                                                                         d.n_composited)
+        assert c["K"] > 0 and c["composited"] > 0 and not c["overflow"]
+    with pytest.raises(puv.PuvError):
+        puv.view_counts(g["R"].state, 2)

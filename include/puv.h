@@ -98,8 +98,17 @@ typedef struct {
 
 typedef struct {
   float bg[3];          /* background colour, composited with T_final (R9) */
-  uint32_t flags;       /* reserved, must be 0 */
+  uint32_t flags;       /* 0, or PUV_RENDER_LPO */
+  /* PUV_RENDER_LPO (NEXT-2 fused into the render): every texel plane value the
+   * render and its backward read is replaced, as it is read, by its LPO proxy -- exactly the value
+   * puv_quantize would write (Q1-Q8): the per-plane range lpo_spec (device, D x 2 floats, from
+   * puv_quant_fit), lpo_pos_bits for the position planes (1..16 or PUV_QUANT_FP16), lpo_attr_bits
+   * (1..16) for the others.  The backward then returns the straight-through (STE) gradient of the
+   * fp32 master planes without a proxy atlas in memory. */
+  const float* lpo_spec;
+  int32_t lpo_pos_bits, lpo_attr_bits;
 } puv_render_opts;
+#define PUV_RENDER_LPO 1u
 
 /* Column layout (R15): L0 at (0,0); levels 1.. stacked top-down at x = cols[0],
  * unrotated; W_A = cols0 + max_{k>=1} cols_k, H_A = max(rows0, sum_{k>=1} rows_k).

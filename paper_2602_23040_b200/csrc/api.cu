@@ -296,6 +296,8 @@ static puv_status fill_planes(const puv_layout* L, const float* const* tab, Plan
   if (!tab) return fail(PUV_E_INVALID_ARGUMENT, "atlas_planes is NULL");
   const bool rho = L->position_mode == PUV_POS_RHO;
   const int n = L->planes + (rho ? 3 : 0);
+  P.qspec = nullptr;
+  for (int d = 0; d < kMaxPlanes; ++d) P.qbits[d] = 0;
   for (int d = 0; d < n; ++d) {
     if (rho && (d == 1 || d == 2)) { P.p[d] = nullptr; continue; }
     if (!tab[d]) return fail(PUV_E_INVALID_ARGUMENT, "atlas plane %d is NULL", d);
@@ -311,7 +313,19 @@ static puv_status prepare(const puv_layout* L, const float* const* atlas_planes,
   if (st) return st;
   st = fill_planes(L, atlas_planes, c.P);
   if (st) return st;
-  if (opts && opts->flags != 0) return fail(PUV_E_UNSUPPORTED, "opts.flags must be 0");
+  if (opts && opts->flags != 0) {
+    if (opts->flags != PUV_RENDER_LPO) return fail(PUV_E_UNSUPPORTED, "opts.flags %u: only PUV_RENDER_LPO", opts->flags);
+    const int pb = opts->lpo_pos_bits, ab = opts->lpo_attr_bits;
+    if (!opts->lpo_spec) return fail(PUV_E_INVALID_ARGUMENT, "PUV_RENDER_LPO without lpo_spec");
+    if ((pb != PUV_QUANT_FP16 && (pb < 1 || pb > 16)) || ab < 1 || ab > 16)
+      return fail(PUV_E_INVALID_ARGUMENT, "LPO bits (%d, %d) outside 1..16 (pos: or PUV_QUANT_FP16)", pb, ab);
+    c.P.qspec = opts->lpo_spec;
+    const bool rho = L->position_mode == PUV_POS_RHO;
+    for (int d = 0; d < L->planes; ++d) {
+      if (rho && (d == 1 || d == 2)) continue;   // unused planes; the ray planes are never quantised
+      c.P.qbits[d] = (int8_t)(d < 3 ? (pb == PUV_QUANT_FP16 ? -1 : pb) : ab);
+    }
+  }
   st = check_cameras(n_views, cams, c.W, c.H);
   if (st) return st;
   if (!state) return fail(PUV_E_INVALID_ARGUMENT, "state is NULL");

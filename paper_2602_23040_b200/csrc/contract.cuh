@@ -6,9 +6,11 @@
 // decisions are bit-identical to the CPU oracle's.  Written from DESIGN.md, not
 // from the oracle's source (they share no code).
 #pragma once
+#include <cuda_fp16.h>
 #include <cstdint>
 
 #include "exp2_table.h"
+#include "internal.cuh"
 
 namespace puv {
 
@@ -75,6 +77,34 @@ PUV_DEV float pair_power(float mx, float my, float ha, float nb, float hc, float
   const float dx = sub(mx, fi), dy = sub(my, fj);
   const float u = fma_(nb, dy, mul(ha, dx));
   return fma_(dx, u, mul(mul(hc, dy), dy));
+}
+
+// LPO fake quantiser (NEXT-2, DESIGN.md §13 Q1-Q8), fp32 contract: code and proxy of one value.
+PUV_DEV void quant1(float x, float mn, float mx, int bits, uint32_t& code, float& prox) {
+  if (bits < 0) {   // reading Q8: IEEE binary16 (round to nearest even); code = its bit pattern
+    const __half h = __float2half_rn(x);
+    code = __half_as_ushort(h);
+    prox = __half2float(h);
+    return;
+  }
+  code = 0;
+  if (mx == mn) { prox = mn; return; }
+  const float L = (float)((1u << bits) - 1u);
+  float t = mul(dvd(sub(x, mn), sub(mx, mn)), L);
+  if (!(t > 0.f)) t = 0.f;
+  if (t > L) t = L;
+  code = (uint32_t)roundf(t);
+  prox = add(mn, mul(dvd((float)code, L), sub(mx, mn)));
+}
+
+// A texel plane value as the render reads it: the master value, or with LPO its proxy.
+PUV_DEV float plane_value(const PlaneTab& P, int d, int g) {
+  const float x = __ldg(P.p[d] + g);
+  if (P.qspec == nullptr || P.qbits[d] == 0) return x;
+  uint32_t code;
+  float prox;
+  quant1(x, __ldg(P.qspec + 2 * d), __ldg(P.qspec + 2 * d + 1), P.qbits[d], code, prox);
+  return prox;
 }
 
 // ---- fp64 value path helpers (not part of the contract) ---------------------------------------

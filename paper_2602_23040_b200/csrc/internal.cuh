@@ -45,7 +45,14 @@ constexpr int kSupT = kSup * kSup;        // tiles per super-tile
 constexpr bool kDirect = PUV_DIRECT != 0;
 constexpr uint32_t kInvisible = 0xFFFFFFFFu;
 
-struct PlaneTab { const float* p[kMaxPlanes]; };
+// Plane table of a render call; with LPO (PUV_RENDER_LPO) every atlas plane value is read through its
+// proxy (qspec = D x (min, max), qbits[d] = bits, -1 = binary16, 0 = read as is; the ray planes of
+// PUV_POS_RHO are never quantised).
+struct PlaneTab {
+  const float* p[kMaxPlanes];
+  const float* qspec;
+  int8_t qbits[kMaxPlanes];
+};
 struct GradTab { float* p[kMaxPlanes]; };
 
 // Per-view camera constants (viewmat rows 0..2, intrinsics, lim = fp32(1.3*W/(2 fx)) (R5)).

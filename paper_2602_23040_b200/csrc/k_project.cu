@@ -23,9 +23,10 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
   const bool occupied = occ == nullptr || occ[g] != 0;
   float mux = 0.f, muy = 0.f, muz = 0.f;
   if (occupied) texel_mu(P, pm, g, mux, muy, muz);
-  const float ls0 = __ldg(P.p[3] + g), ls1 = __ldg(P.p[4] + g), ls2 = __ldg(P.p[5] + g);
-  const float qw = __ldg(P.p[6] + g), qx = __ldg(P.p[7] + g), qy = __ldg(P.p[8] + g), qz = __ldg(P.p[9] + g);
-  const float logit = __ldg(P.p[10] + g);
+  const float ls0 = plane_value(P, 3, g), ls1 = plane_value(P, 4, g), ls2 = plane_value(P, 5, g);
+  const float qw = plane_value(P, 6, g), qx = plane_value(P, 7, g), qy = plane_value(P, 8, g),
+              qz = plane_value(P, 9, g);
+  const float logit = plane_value(P, 10, g);
   const Unpacked u = unpack_contract(ls0, ls1, ls2, qw, qx, qy, qz, logit);
   bool any = false;
   Unpacked64 u64;
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
       any = true;
       u64 = unpack64(ls0, ls1, ls2, qw, qx, qy, qz, logit);
 #pragma unroll
-      for (int k = 0; k < 3 * NK; ++k) sh[k] = __ldg(P.p[11 + k] + g);
+      for (int k = 0; k < 3 * NK; ++k) sh[k] = plane_value(P, 11 + k, g);
     }
     const Proj64 p64 = project64(c, mux, muy, muz, u64, cp.clx, cp.cly);
     // SH colour (R3) in fp64; the clamp decision is recorded for K7

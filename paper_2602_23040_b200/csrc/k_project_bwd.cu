@@ -33,9 +33,10 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
   float fmx, fmy, fmz;
   texel_mu(P, pm, g, fmx, fmy, fmz);   // the fp32 position the render saw (xyz or c (+) rho (x) ray)
   const double mux = fmx, muy = fmy, muz = fmz;
-  const float ls0 = __ldg(P.p[3] + g), ls1 = __ldg(P.p[4] + g), ls2 = __ldg(P.p[5] + g);
-  const float qw = __ldg(P.p[6] + g), qx = __ldg(P.p[7] + g), qy = __ldg(P.p[8] + g), qz = __ldg(P.p[9] + g);
-  const float logit = __ldg(P.p[10] + g);
+  const float ls0 = plane_value(P, 3, g), ls1 = plane_value(P, 4, g), ls2 = plane_value(P, 5, g);
+  const float qw = plane_value(P, 6, g), qx = plane_value(P, 7, g), qy = plane_value(P, 8, g),
+              qz = plane_value(P, 9, g);
+  const float logit = plane_value(P, 10, g);
   const Unpacked64 u = unpack64(ls0, ls1, ls2, qw, qx, qy, qz, logit);
 
   double dmu0 = 0, dmu1 = 0, dmu2 = 0, dop = 0;
@@ -121,8 +122,8 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
       double dd0 = 0, dd1 = 0, dd2 = 0;
 #pragma unroll
       for (int k = 1; k < NK; ++k) {
-        const double w = (double)__ldg(P.p[11 + 3 * k] + g) * drgb[0] + (double)__ldg(P.p[12 + 3 * k] + g) * drgb[1] +
-                         (double)__ldg(P.p[13 + 3 * k] + g) * drgb[2];
+        const double w = (double)plane_value(P, 11 + 3 * k, g) * drgb[0] +
+                         (double)plane_value(P, 12 + 3 * k, g) * drgb[1] + (double)plane_value(P, 13 + 3 * k, g) * drgb[2];
         dd0 = fma(w, dY[k][0], dd0);
         dd1 = fma(w, dY[k][1], dd1);
         dd2 = fma(w, dY[k][2], dd2);

@@ -90,23 +90,6 @@ struct QPlanes {
   int8_t bits[kMaxPlanes];   // 0: plane not quantised (rho mode's unused planes 1, 2); -1: binary16
 };
 
-PUV_DEV void quant1(float x, float mn, float mx, int bits, uint32_t& code, float& prox) {
-  if (bits < 0) {   // reading Q8: IEEE binary16 (round to nearest even); code = its bit pattern
-    const __half h = __float2half_rn(x);
-    code = __half_as_ushort(h);
-    prox = __half2float(h);
-    return;
-  }
-  code = 0;
-  if (mx == mn) { prox = mn; return; }
-  const float L = (float)((1u << bits) - 1u);
-  float t = mul(dvd(sub(x, mn), sub(mx, mn)), L);
-  if (!(t > 0.f)) t = 0.f;
-  if (t > L) t = L;
-  code = (uint32_t)roundf(t);
-  prox = add(mn, mul(dvd((float)code, L), sub(mx, mn)));
-}
-
 // 4 texels per thread (float4 / uchar4 / ushort4 accesses); N % 4 == 0 and 16-byte aligned planes.
 __global__ void __launch_bounds__(256) k_quantize4(QPlanes Q, int D, const float* __restrict__ spec,
                                                    const uint8_t* __restrict__ occ, int64_t n4) {

@@ -52,8 +52,12 @@ class Camera(C.Structure):
                 ("campos", C.c_float * 3)]
 
 
+RENDER_LPO = 1
+
+
 class RenderOpts(C.Structure):
-    _fields_ = [("bg", C.c_float * 3), ("flags", C.c_uint32)]
+    _fields_ = [("bg", C.c_float * 3), ("flags", C.c_uint32), ("lpo_spec", C.c_void_p), ("lpo_pos_bits", C.c_int32),
+                ("lpo_attr_bits", C.c_int32)]
 
 
 class ViewDebug(C.Structure):
@@ -208,10 +212,20 @@ def cameras(cams) -> C.Array:
     return arr
 
 
-def opts(bg=(0.0, 0.0, 0.0)) -> RenderOpts:
+def opts(bg=(0.0, 0.0, 0.0), lpo=None) -> RenderOpts:
+    """Render options.  lpo = (spec, pos_bits, attr_bits): render the LPO proxy of the atlas inline
+    (PUV_RENDER_LPO; spec = quant_fit's (D, 2) CUDA tensor, kept alive by the caller; pos_bits may be
+    "fp16"); the backward then gives the STE gradient of the master planes."""
     o = RenderOpts()
     o.bg[:] = [float(x) for x in bg]
     o.flags = 0
+    if lpo is not None:
+        spec, pb, ab = lpo
+        assert spec.is_cuda and spec.dtype == torch.float32 and spec.is_contiguous()
+        o.flags = RENDER_LPO
+        o.lpo_spec = spec.data_ptr()
+        o.lpo_pos_bits = QUANT_FP16 if pb == "fp16" else int(pb)
+        o.lpo_attr_bits = int(ab)
     return o
 
 
@@ -590,10 +604,10 @@ def debug_tensors(layout, cams, state, arena, view):
 class Renderer:
     """Owns the per-call state and key arena for a fixed (layout, cameras) signature."""
 
-    def __init__(self, layout: Layout, cams, bg=(0.0, 0.0, 0.0), device="cuda", arena_bytes=None):
+    def __init__(self, layout: Layout, cams, bg=(0.0, 0.0, 0.0), device="cuda", arena_bytes=None, lpo=None):
         self.layout = layout
         self.cams = cams
-        self.opts = opts(bg)
+        self.opts = opts(bg, lpo)
         self.device = torch.device(device)
         sb, hint = query_sizes(layout, cams, self.opts)
         self.state = torch.empty(sb, dtype=torch.uint8, device=self.device)

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_sizes_match_header():
     assert C.sizeof(puv.Camera) == 16 * 4 + 4 * 4 + 2 * 4 + 4 + 3 * 4
     assert C.sizeof(puv.Layout) == 5 * 4 + 16 * 5 * 4 + 4 + 3 * 4
-    assert C.sizeof(puv.RenderOpts) == 16
+    assert C.sizeof(puv.RenderOpts) == 16 + 8 + 2 * 4   # bg, flags, lpo_spec, lpo_pos_bits, lpo_attr_bits
 
 
 @pytest.mark.parametrize("shapes", [[(64, 64)], [(512, 512), (256, 256), (128, 128)], [(1024, 1024), (1024, 512)],

@@ -98,9 +98,12 @@ PUV_DEV void quant1(float x, float mn, float mx, int bits, uint32_t& code, float
 }
 
 // A texel plane value as the render reads it: the master value, or with LPO its proxy.
+// LPO = true only in the PUV_RENDER_LPO instantiations of K1 / K7 (the plain kernels stay free of the
+// quantiser code: compiled in, it cost the plain K1 +1.4 ms per C3 step in an A/B).
+template <bool LPO>
 PUV_DEV float plane_value(const PlaneTab& P, int d, int g) {
   const float x = __ldg(P.p[d] + g);
-  if (P.qspec == nullptr || P.qbits[d] == 0) return x;
+  if (!LPO || P.qbits[d] == 0) return x;
   uint32_t code;
   float prox;
   quant1(x, __ldg(P.qspec + 2 * d), __ldg(P.qspec + 2 * d + 1), P.qbits[d], code, prox);

@@ -11,7 +11,7 @@
 
 namespace puv {
 
-template <int DEG>
+template <int DEG, bool LPO>
 #ifndef PUV_PROJ_MINB
 #define PUV_PROJ_MINB 3
 #endif
@@ -22,11 +22,11 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
   constexpr int NK = (DEG + 1) * (DEG + 1);
   const bool occupied = occ == nullptr || occ[g] != 0;
   float mux = 0.f, muy = 0.f, muz = 0.f;
-  if (occupied) texel_mu(P, pm, g, mux, muy, muz);
-  const float ls0 = plane_value(P, 3, g), ls1 = plane_value(P, 4, g), ls2 = plane_value(P, 5, g);
-  const float qw = plane_value(P, 6, g), qx = plane_value(P, 7, g), qy = plane_value(P, 8, g),
-              qz = plane_value(P, 9, g);
-  const float logit = plane_value(P, 10, g);
+  if (occupied) texel_mu<LPO>(P, pm, g, mux, muy, muz);
+  const float ls0 = plane_value<LPO>(P, 3, g), ls1 = plane_value<LPO>(P, 4, g), ls2 = plane_value<LPO>(P, 5, g);
+  const float qw = plane_value<LPO>(P, 6, g), qx = plane_value<LPO>(P, 7, g), qy = plane_value<LPO>(P, 8, g),
+              qz = plane_value<LPO>(P, 9, g);
+  const float logit = plane_value<LPO>(P, 10, g);
   const Unpacked u = unpack_contract(ls0, ls1, ls2, qw, qx, qy, qz, logit);
   bool any = false;
   Unpacked64 u64;
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
       any = true;
       u64 = unpack64(ls0, ls1, ls2, qw, qx, qy, qz, logit);
 #pragma unroll
-      for (int k = 0; k < 3 * NK; ++k) sh[k] = plane_value(P, 11 + k, g);
+      for (int k = 0; k < 3 * NK; ++k) sh[k] = plane_value<LPO>(P, 11 + k, g);
     }
     const Proj64 p64 = project64(c, mux, muy, muz, u64, cp.clx, cp.cly);
     // SH colour (R3) in fp64; the clamp decision is recorded for K7
@@ -89,12 +89,15 @@ void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint
                     cudaStream_t s) {
   const int threads = 128;
   const int blocks = (p.N + threads - 1) / threads;
+#define PUV_K1(D, L) k_project<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy)
+  const bool lpo = P.qspec != nullptr;
   switch (p.deg) {
-    case 0: k_project<0><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
-    case 1: k_project<1><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
-    case 2: k_project<2><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
-    default: k_project<3><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy); break;
+    case 0: if (lpo) PUV_K1(0, true); else PUV_K1(0, false); break;
+    case 1: if (lpo) PUV_K1(1, true); else PUV_K1(1, false); break;
+    case 2: if (lpo) PUV_K1(2, true); else PUV_K1(2, false); break;
+    default: if (lpo) PUV_K1(3, true); else PUV_K1(3, false); break;
   }
+#undef PUV_K1
   count_launches(1);
 }
 

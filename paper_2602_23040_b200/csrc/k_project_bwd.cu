@@ -15,7 +15,7 @@
 
 namespace puv {
 
-template <int DEG>
+template <int DEG, bool LPO>
 #ifndef PUV_PBWD_MINB
 #define PUV_PBWD_MINB 1
 #endif
@@ -31,12 +31,12 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
   if (!any) return;
 
   float fmx, fmy, fmz;
-  texel_mu(P, pm, g, fmx, fmy, fmz);   // the fp32 position the render saw (xyz or c (+) rho (x) ray)
+  texel_mu<LPO>(P, pm, g, fmx, fmy, fmz);   // the fp32 position the render saw (xyz or c (+) rho (x) ray)
   const double mux = fmx, muy = fmy, muz = fmz;
-  const float ls0 = plane_value(P, 3, g), ls1 = plane_value(P, 4, g), ls2 = plane_value(P, 5, g);
-  const float qw = plane_value(P, 6, g), qx = plane_value(P, 7, g), qy = plane_value(P, 8, g),
-              qz = plane_value(P, 9, g);
-  const float logit = plane_value(P, 10, g);
+  const float ls0 = plane_value<LPO>(P, 3, g), ls1 = plane_value<LPO>(P, 4, g), ls2 = plane_value<LPO>(P, 5, g);
+  const float qw = plane_value<LPO>(P, 6, g), qx = plane_value<LPO>(P, 7, g), qy = plane_value<LPO>(P, 8, g),
+              qz = plane_value<LPO>(P, 9, g);
+  const float logit = plane_value<LPO>(P, 10, g);
   const Unpacked64 u = unpack64(ls0, ls1, ls2, qw, qx, qy, qz, logit);
 
   double dmu0 = 0, dmu1 = 0, dmu2 = 0, dop = 0;
@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
       double dd0 = 0, dd1 = 0, dd2 = 0;
 #pragma unroll
       for (int k = 1; k < NK; ++k) {
-        const double w = (double)plane_value(P, 11 + 3 * k, g) * drgb[0] +
-                         (double)plane_value(P, 12 + 3 * k, g) * drgb[1] + (double)plane_value(P, 13 + 3 * k, g) * drgb[2];
+        const double w = (double)plane_value<LPO>(P, 11 + 3 * k, g) * drgb[0] +
+                         (double)plane_value<LPO>(P, 12 + 3 * k, g) * drgb[1] + (double)plane_value<LPO>(P, 13 + 3 * k, g) * drgb[2];
         dd0 = fma(w, dY[k][0], dd0);
         dd1 = fma(w, dY[k][1], dd1);
         dd2 = fma(w, dY[k][2], dd2);
@@ -186,12 +186,15 @@ void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const 
                         const CamBatch& cb, const GradTab& G, cudaStream_t s) {
   const int threads = 128;
   const int blocks = (p.N + threads - 1) / threads;
+#define PUV_K7(D, L) k_project_bwd<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G)
+  const bool lpo = P.qspec != nullptr;
   switch (p.deg) {
-    case 0: k_project_bwd<0><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
-    case 1: k_project_bwd<1><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
-    case 2: k_project_bwd<2><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
-    default: k_project_bwd<3><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G); break;
+    case 0: if (lpo) PUV_K7(0, true); else PUV_K7(0, false); break;
+    case 1: if (lpo) PUV_K7(1, true); else PUV_K7(1, false); break;
+    case 2: if (lpo) PUV_K7(2, true); else PUV_K7(2, false); break;
+    default: if (lpo) PUV_K7(3, true); else PUV_K7(3, false); break;
   }
+#undef PUV_K7
   count_launches(1);
 }
 

@@ -12,16 +12,17 @@
 namespace puv {
 
 // Texel position (a1): explicit xyz planes, or mu = c (+) rho (x) ray in the fp32 contract (PUV_POS_RHO).
+template <bool LPO = false>
 PUV_DEV void texel_mu(const PlaneTab& P, const PosMode& pm, int g, float& x, float& y, float& z) {
   if (pm.rho) {
-    const float r = plane_value(P, 0, g);
+    const float r = plane_value<LPO>(P, 0, g);
     x = add(pm.c[0], mul(r, __ldg(P.p[pm.D] + g)));
     y = add(pm.c[1], mul(r, __ldg(P.p[pm.D + 1] + g)));
     z = add(pm.c[2], mul(r, __ldg(P.p[pm.D + 2] + g)));
   } else {
-    x = plane_value(P, 0, g);
-    y = plane_value(P, 1, g);
-    z = plane_value(P, 2, g);
+    x = plane_value<LPO>(P, 0, g);
+    y = plane_value<LPO>(P, 1, g);
+    z = plane_value<LPO>(P, 2, g);
   }
 }
 

@@ -319,6 +319,22 @@ puv_status puv_train_step_host(const puv_layout* layout, const float* const* atl
                                float* const* atlas_grad, const puv_copy* downloads, int32_t n_downloads,
                                void* stream);
 
+/* puv_train_step from HOST buffers with the host link overlapped (the e2e path of a training loop):
+ * atlas_host (host, D x H_A*W_A floats, plane-major) is uploaded into the device planes atlas_planes
+ * (a host table; rho mode's unused planes 1, 2 may be NULL and the ray planes stay resident) in 4
+ * texel chunks on an internal copy stream, K1 projecting each chunk as soon as it has landed; the
+ * targets follow on that stream (the first loss waits for them); the gradient (OVERWRITTEN in
+ * atlas_grad) goes back into grad_host (host, D x H_A*W_A) in 4 texel chunks on a second copy
+ * stream as K7 finishes each, then the loss into *loss_host.  Same results as puv_train_step.
+ * Asynchronous: synchronise `stream` before reading grad_host / loss_host (pinned memory makes the
+ * copies asynchronous).  Every argument is checked before anything is enqueued. */
+puv_status puv_train_step_host_atlas(const puv_layout* layout, float* const* atlas_planes, const float* atlas_host,
+                                     const uint8_t* atlas_occ, int32_t n_views, const puv_camera* cams,
+                                     const puv_render_opts* opts, const float* targets_host, float* targets,
+                                     const uint8_t* dynamic_mask, int32_t views_per_call,
+                                     const puv_step_buffers* buffers, float* const* atlas_grad, float* grad_host,
+                                     double* loss_host, void* stream);
+
 /* The one host synchronisation per step: waits for `stream`, then reports
  * whether any view of the last render overflowed the arena and the arena
  * bytes the call needs.  Host outputs. */

@@ -78,7 +78,8 @@ struct StreamSet {
   std::mutex mu;
   cudaStream_t s[kBinStreams] = {};
   cudaStream_t s2 = nullptr;     // per-view loss + composite backward of the fused L2 step
-  cudaStream_t cp = nullptr;     // host->device target uploads of puv_train_step_host
+  cudaStream_t cp = nullptr;     // host->device uploads of the host-buffer steps
+  cudaStream_t cp2 = nullptr;    // device->host downloads of puv_train_step_host_atlas
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> ev, fev;
   static cudaEvent_t pooled(std::vector<cudaEvent_t>& pool, int v) {
@@ -113,6 +114,7 @@ static StreamSet& stream_set(int /*n*/) {
     cudaEventCreateWithFlags(&ss->join, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ss->s2, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&ss->cp, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ss->cp2, cudaStreamNonBlocking);
     sets[dev] = ss;
   }
   return *sets[dev];
@@ -491,9 +493,20 @@ struct L2Hook {
 
 // Project, bin and composite all views of a call (rows a1-a5); with `hook`, also rows a6-a7 per
 // view.  `s` is ordered after everything enqueued here when the function returns.
+// Host-link overlap of puv_train_step_host_atlas: the atlas arrives in texel chunks and K1 projects
+// each chunk once it has landed (`ready`); the gradient leaves in texel chunks, each copied out
+// as soon as K7 has finished it (`done`).
+constexpr int kTexelChunks = 4;
+struct TexelPipe {
+  int n;                              // chunks (<= kTexelChunks)
+  int bound[kTexelChunks + 1];        // texel ranges [bound[i], bound[i+1])
+  cudaEvent_t ready[kTexelChunks];    // K1 of chunk i waits for it (nullable)
+  cudaEvent_t done[kTexelChunks];     // recorded after K7 of chunk i (nullable)
+};
+
 static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_views, const puv_camera* cams,
                             const float bg[3], float* images, void* state, void* arena, size_t arena_bytes,
-                            cudaStream_t s, const L2Hook* hook) {
+                            cudaStream_t s, const L2Hook* hook, const TexelPipe* tin = nullptr) {
   const Plan& p = c.plan;
   cudaMemsetAsync(c.views.hdr, 0, sizeof(ViewHdr) * n_views, s);
   launch_begin_call(p, c.views, arena_bytes / 4, s);
@@ -503,7 +516,14 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
     cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
     for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
     StageScope sc(PUV_STAGE_PROJECT, s);
-    launch_project(p, c.views, c.P, atlas_occ, cb, s);
+    if (tin) {
+      for (int i = 0; i < tin->n; ++i) {
+        if (tin->ready[i]) cudaStreamWaitEvent(s, tin->ready[i], 0);
+        launch_project(p, c.views, c.P, atlas_occ, cb, s, tin->bound[i], tin->bound[i + 1]);
+      }
+    } else {
+      launch_project(p, c.views, c.P, atlas_occ, cb, s);
+    }
   }
   // Pipeline: view v is depth-sorted and binned on binning stream v % nscratch (its own scratch
   // block) while earlier views composite on `s`; `s` waits on view v's binning event only.
@@ -682,14 +702,20 @@ static puv_status grad_table(const puv_layout* layout, float* const* atlas_grad,
 
 // K7 over all views of the call, in camera batches (rows a8, a9)
 static void project_backward(const Common& c, const uint8_t* atlas_occ, int n_views, const puv_camera* cams,
-                             const uint8_t* dynamic_mask, const GradTab& G, cudaStream_t s) {
-  for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
-    CamBatch cb;
-    cb.v0 = v0;
-    cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
-    for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
-    StageScope sc(PUV_STAGE_PROJECT_BWD, s);
-    launch_project_bwd(c.plan, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s);
+                             const uint8_t* dynamic_mask, const GradTab& G, cudaStream_t s,
+                             const TexelPipe* tout = nullptr) {
+  const int nchunk = tout ? tout->n : 1;
+  for (int k = 0; k < nchunk; ++k) {
+    const int g0 = tout ? tout->bound[k] : 0, g1 = tout ? tout->bound[k + 1] : -1;
+    for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
+      CamBatch cb;
+      cb.v0 = v0;
+      cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
+      for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
+      StageScope sc(PUV_STAGE_PROJECT_BWD, s);
+      launch_project_bwd(c.plan, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s, g0, g1);
+    }
+    if (tout && tout->done[k]) cudaEventRecord(tout->done[k], s);
   }
 }
 
@@ -744,7 +770,8 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
                                      const uint8_t* atlas_occ, int32_t n_views, const puv_camera* cams,
                                      const puv_render_opts* opts, const float* targets, const uint8_t* dynamic_mask,
                                      int32_t views_per_call, const puv_step_buffers* b, float* const* atlas_grad,
-                                     cudaEvent_t targets_ready, cudaStream_t s, bool validate_only = false) {
+                                     cudaEvent_t targets_ready, cudaStream_t s, bool validate_only = false,
+                                     const TexelPipe* tin = nullptr, const TexelPipe* tout = nullptr) {
   if (!b) return fail(PUV_E_INVALID_ARGUMENT, "buffers is NULL");
   if (!targets || !b->images || !b->dL_dimages || !b->loss || !b->overflow || !b->arena_need)
     return fail(PUV_E_INVALID_ARGUMENT, "NULL targets / images / dL_dimages / loss / overflow / arena_need");
@@ -774,11 +801,12 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
     // of K6's moment slots there too: both overlap the compositing of later views
     const L2Hook hook{targets + (size_t)v0 * HW3, b->dL_dimages, b->loss, v0 == 0 ? targets_ready : nullptr, false,
                       cc.views.grad2d, (size_t)72 * n * cc.plan.N};
-    render_pipeline(cc, atlas_occ, n, cams + v0, bg, b->images, b->state, b->arena, b->arena_bytes, s, &hook);
+    render_pipeline(cc, atlas_occ, n, cams + v0, bg, b->images, b->state, b->arena, b->arena_bytes, s, &hook,
+                    v0 == 0 ? tin : nullptr);
     launch_overflow_acc(b->state, b->overflow, b->arena_need, s);
     { StageScope sc(PUV_STAGE_RASTER_BWD, s);
       launch_raster_bwd(cc.plan, cc.views, (const uint32_t*)b->arena, b->dL_dimages, 0, n, s); }
-    project_backward(cc, atlas_occ, n, cams + v0, dynamic_mask, G, s);
+    project_backward(cc, atlas_occ, n, cams + v0, dynamic_mask, G, s, v0 + n >= n_views ? tout : nullptr);
   }
   return PUV_OK;
 }
@@ -842,6 +870,80 @@ puv_status puv_train_step_host(const puv_layout* layout, const float* const* atl
     if (downloads[i].bytes)
       cudaMemcpyAsync(downloads[i].dst, downloads[i].src, downloads[i].bytes, cudaMemcpyDeviceToHost, s);
   return cuda_check("puv_train_step_host");
+}
+
+puv_status puv_train_step_host_atlas(const puv_layout* layout, float* const* atlas_planes, const float* atlas_host,
+                                     const uint8_t* atlas_occ, int32_t n_views, const puv_camera* cams,
+                                     const puv_render_opts* opts, const float* targets_host, float* targets,
+                                     const uint8_t* dynamic_mask, int32_t views_per_call,
+                                     const puv_step_buffers* buffers, float* const* atlas_grad, float* grad_host,
+                                     double* loss_host, void* stream) {
+  if (!atlas_host || !grad_host || !loss_host || !targets_host || !targets || !atlas_planes)
+    return fail(PUV_E_INVALID_ARGUMENT, "NULL host / device buffer");
+  int W, H;
+  puv_status st = check_cameras(n_views, cams, W, H);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  st = train_step_enqueue(layout, (const float* const*)atlas_planes, atlas_occ, n_views, cams, opts, targets,
+                          dynamic_mask, views_per_call, buffers, atlas_grad, nullptr, s, true);
+  if (st) return st;
+  const size_t N = (size_t)layout->atlas_w * layout->atlas_h;
+  const int D = layout->planes;
+  StreamSet& ss = stream_set(1);
+  TexelPipe tin{}, tout{};
+  tin.n = tout.n = kTexelChunks;
+  for (int i = 0; i <= kTexelChunks; ++i) tin.bound[i] = tout.bound[i] = (int)((N * (size_t)i) / kTexelChunks);
+  cudaEvent_t fork = nullptr, tdone = nullptr, gdone = nullptr;
+  cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&tdone, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&gdone, cudaEventDisableTiming);
+  for (int i = 0; i < kTexelChunks; ++i) {
+    cudaEventCreateWithFlags(&tin.ready[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&tout.done[i], cudaEventDisableTiming);
+  }
+  {
+    std::lock_guard<std::mutex> lock(ss.mu);   // the copy streams are shared per device
+    cudaEventRecord(fork, s);                  // after earlier work on `s` (the buffers are free)
+    cudaStreamWaitEvent(ss.cp, fork, 0);
+    // the atlas planes in texel chunks (K1 projects a chunk as soon as it has landed), then the targets
+    for (int i = 0; i < kTexelChunks; ++i) {
+      const size_t g0 = tin.bound[i], n = tin.bound[i + 1] - g0;
+      for (int d = 0; d < D; ++d)
+        if (atlas_planes[d])
+          cudaMemcpyAsync(atlas_planes[d] + g0, atlas_host + (size_t)d * N + g0, n * sizeof(float),
+                          cudaMemcpyHostToDevice, ss.cp);
+      cudaEventRecord(tin.ready[i], ss.cp);
+    }
+    cudaMemcpyAsync(targets, targets_host, (size_t)n_views * 3 * W * H * sizeof(float), cudaMemcpyHostToDevice,
+                    ss.cp);
+    cudaEventRecord(tdone, ss.cp);
+  }
+  st = train_step_enqueue(layout, (const float* const*)atlas_planes, atlas_occ, n_views, cams, opts, targets,
+                          dynamic_mask, views_per_call, buffers, atlas_grad, tdone, s, false, &tin, &tout);
+  if (!st) {
+    std::lock_guard<std::mutex> lock(ss.mu);
+    // the gradient in texel chunks as K7 finishes each, then the loss; `s` waits for all of it
+    for (int i = 0; i < kTexelChunks; ++i) {
+      cudaStreamWaitEvent(ss.cp2, tout.done[i], 0);
+      const size_t g0 = tout.bound[i], n = tout.bound[i + 1] - g0;
+      for (int d = 0; d < D; ++d)
+        if (atlas_grad[d])
+          cudaMemcpyAsync(grad_host + (size_t)d * N + g0, atlas_grad[d] + g0, n * sizeof(float),
+                          cudaMemcpyDeviceToHost, ss.cp2);
+    }
+    cudaMemcpyAsync(loss_host, buffers->loss, sizeof(double), cudaMemcpyDeviceToHost, ss.cp2);
+    cudaEventRecord(gdone, ss.cp2);
+    cudaStreamWaitEvent(s, gdone, 0);
+  }
+  cudaEventDestroy(fork);
+  cudaEventDestroy(tdone);
+  cudaEventDestroy(gdone);
+  for (int i = 0; i < kTexelChunks; ++i) {
+    cudaEventDestroy(tin.ready[i]);
+    cudaEventDestroy(tout.done[i]);
+  }
+  if (st) return st;
+  return cuda_check("puv_train_step_host_atlas");
 }
 
 puv_status puv_check_overflow(const void* state, int32_t n_views, void* stream, int32_t* overflowed,

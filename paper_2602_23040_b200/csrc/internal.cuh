@@ -155,7 +155,7 @@ size_t bin_scratch_bytes(size_t N, int ntiles);
 
 // ---- launchers (all asynchronous on `s`) ----
 void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,
-                    cudaStream_t s);
+                    cudaStream_t s, int g0 = 0, int g1 = -1);
 void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cudaStream_t s);
 void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s, bool level2);
 void launch_bin_level2(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
@@ -164,7 +164,7 @@ void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, flo
 void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int view0,
                        int n_views, cudaStream_t s);
 void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const uint8_t* mask,
-                        const CamBatch& cb, const GradTab& G, cudaStream_t s);
+                        const CamBatch& cb, const GradTab& G, cudaStream_t s, int g0 = 0, int g1 = -1);
 void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s,
                     bool accumulate);
 void launch_pack(const puv_layout& L, const float* const* level_planes, const uint8_t* const* level_occ,

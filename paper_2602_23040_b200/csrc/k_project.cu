@@ -16,9 +16,10 @@ template <int DEG, bool LPO>
 #define PUV_PROJ_MINB 3
 #endif
 __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ, int N,
-                                                 const __grid_constant__ CamBatch cb, Views v, int gx, int gy) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= N) return;
+                                                 const __grid_constant__ CamBatch cb, Views v, int gx, int gy,
+                                                 int g0, int g1) {
+  const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;   // texels [g0, g1) of the N
+  if (g >= g1) return;
   constexpr int NK = (DEG + 1) * (DEG + 1);
   const bool occupied = occ == nullptr || occ[g] != 0;
   float mux = 0.f, muy = 0.f, muz = 0.f;
@@ -86,10 +87,12 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
 }
 
 void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,
-                    cudaStream_t s) {
+                    cudaStream_t s, int g0, int g1) {
+  if (g1 < 0) g1 = p.N;
+  if (g1 <= g0) return;
   const int threads = 128;
-  const int blocks = (p.N + threads - 1) / threads;
-#define PUV_K1(D, L) k_project<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy)
+  const int blocks = (g1 - g0 + threads - 1) / threads;
+#define PUV_K1(D, L) k_project<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, p.N, cb, v, p.gx, p.gy, g0, g1)
   const bool lpo = P.qspec != nullptr;
   switch (p.deg) {
     case 0: if (lpo) PUV_K1(0, true); else PUV_K1(0, false); break;

@@ -21,9 +21,10 @@ template <int DEG, bool LPO>
 #endif
 __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ,
                                                     const uint8_t* __restrict__ mask, int N,
-                                                    const __grid_constant__ CamBatch cb, Views v, GradTab Gt) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= N) return;
+                                                    const __grid_constant__ CamBatch cb, Views v, GradTab Gt,
+                                                    int g0, int g1) {
+  const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;   // texels [g0, g1) of the N
+  if (g >= g1) return;
   if (occ != nullptr && occ[g] == 0) return;
   constexpr int NK = (DEG + 1) * (DEG + 1);
   bool any = false;
@@ -183,10 +184,12 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
 }
 
 void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const uint8_t* mask,
-                        const CamBatch& cb, const GradTab& G, cudaStream_t s) {
+                        const CamBatch& cb, const GradTab& G, cudaStream_t s, int g0, int g1) {
+  if (g1 < 0) g1 = p.N;
+  if (g1 <= g0) return;
   const int threads = 128;
-  const int blocks = (p.N + threads - 1) / threads;
-#define PUV_K7(D, L) k_project_bwd<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G)
+  const int blocks = (g1 - g0 + threads - 1) / threads;
+#define PUV_K7(D, L) k_project_bwd<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G, g0, g1)
   const bool lpo = P.qspec != nullptr;
   switch (p.deg) {
     case 0: if (lpo) PUV_K7(0, true); else PUV_K7(0, false); break;

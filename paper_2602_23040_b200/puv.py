@@ -111,6 +111,8 @@ def lib():
         L.puv_overflow_accumulate.argtypes = [P, P, P, P]
         L.puv_train_step.argtypes = [P, P, P, S, P, P, P, P, S, P, P, P]
         L.puv_train_step_host.argtypes = [P, P, P, S, P, P, P, S, P, P, P, S, P, P, P, S, P]
+        L.puv_train_step_host_atlas.argtypes = [P, P, P, P, S, P, P, P, P, P, S, P, P, P, P, P]
+        L.puv_train_step_host_atlas.restype = C.c_int32
         L.puv_debug_view.argtypes = [P, S, P, P, C.c_size_t, P, S, P, P]
         L.puv_debug_contract.argtypes = [S, P, P, C.c_int64, P]
         L.puv_view_counts.argtypes = [P, S, P, P]
@@ -506,6 +508,22 @@ def train_step_host(layout, atlas, occ, cams, targets_host, targets, grad, st: S
     _ok(lib().puv_train_step_host(C.byref(layout), _planes(atlas), _ptr(occ), len(cams), cams, C.byref(st.opts), up,
                                   nu, _ptr(targets_host), _ptr(targets), _ptr(mask), st.views_per_call,
                                   C.byref(st.buffers()), _planes(grad), down, nd, _stream(stream)))
+
+
+def train_step_host_atlas(layout, atlas_dev, atlas_host, occ, cams, targets_host, targets, grad, grad_host, loss_host,
+                          st: StepState, mask=None, stream=None):
+    """puv_train_step_host_atlas: atlas_host -> atlas_dev and grad -> grad_host in texel chunks overlapping
+    K1 / K7, targets_host -> targets beside the render, the loss into loss_host (all host tensors pinned,
+    contiguous; atlas_host / grad_host (D, H_A, W_A) fp32, loss_host (1,) fp64)."""
+    _check_images("targets", targets, len(cams), cams)
+    for name, t in (("atlas_host", atlas_host), ("grad_host", grad_host), ("targets_host", targets_host)):
+        assert not t.is_cuda and t.is_contiguous() and t.dtype == torch.float32, f"{name}: contiguous fp32 host"
+    assert atlas_host.numel() == grad_host.numel() == layout.planes * layout.atlas_w * layout.atlas_h
+    assert not loss_host.is_cuda and loss_host.dtype == torch.float64
+    _ok(lib().puv_train_step_host_atlas(C.byref(layout), _planes(atlas_dev), _ptr(atlas_host), _ptr(occ), len(cams),
+                                        cams, C.byref(st.opts), _ptr(targets_host), _ptr(targets), _ptr(mask),
+                                        st.views_per_call, C.byref(st.buffers()), _planes(grad), _ptr(grad_host),
+                                        _ptr(loss_host), _stream(stream)))
 
 
 def check_overflow(state, n_views, stream=None):

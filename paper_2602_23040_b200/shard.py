@@ -106,9 +106,12 @@ class ShardedStep:
         render, and the result -- the gradient planes and the loss -- is copied back into
         `grad_host` / `loss_host`.  With world > 1 the download follows the all-reduce.  Host
         tensors should be pinned (asynchronous copies).  Synchronise before reading the results."""
-        downloads = [(grad, grad_host), (self.st.loss, loss_host)] if self.world == 1 else []
+        if self.world == 1:   # uploads and downloads in texel chunks overlapping K1 / K7
+            puv.train_step_host_atlas(self.layout, atlas_dev, atlas_host, occ, self.cams, targets_host, targets_dev,
+                                      grad, grad_host, loss_host, self.st, mask=mask)
+            return loss_host
         puv.train_step_host(self.layout, atlas_dev, occ, self.cams, targets_host, targets_dev, grad, self.st,
-                            uploads=[(atlas_host, atlas_dev)], downloads=downloads, mask=mask)
+                            uploads=[(atlas_host, atlas_dev)], downloads=[], mask=mask)
         if self.world > 1:
             reduce_gradients(grad, self.st.loss, self.world, self.group)
             grad_host.copy_(grad, non_blocking=True)

@@ -6,7 +6,8 @@
   bit-identical to the world-1 run (the forward has no atomics); the exchanged
   gradient is the fp32 sum of the two ranks' local gradients; it equals the world-1 gradient up
   to that summation order and the oracle's at the north_star tolerance (+ the same allowance).
-* `step_host` (puv_train_step_host: host inputs in, gradient + loss out) equals `step`.
+* `step_host` (puv_train_step_host_atlas: host atlas and targets in, gradient + loss out, the
+  copies overlapping K1 / K7 in texel chunks) and the generic puv_train_step_host equal `step`.
 * View chunks (views_per_call) equal one call up to the fp32 rounding of each chunk's sum."""
 import os
 import socket
@@ -123,6 +124,14 @@ def test_step_host_equals_step_c2():
         assert abs(loss_host.item() - loss) <= 1e-12 * loss   # fp64 partial sums, atomic order
         g = grad_host.numpy()
         assert np.all(np.abs(g - g_dev) <= np.maximum(1e-6 * np.abs(g_dev), 1e-12))
+    # the generic host-buffer call (upload / download lists) gives the same
+    grad_host.zero_()
+    loss_host.zero_()
+    puv.train_step_host(layout, a_dev, occ, st.cams, tg_host, t_dev, grad, st.st, uploads=[(atlas_host, a_dev)],
+                        downloads=[(grad, grad_host), (st.st.loss, loss_host)])
+    torch.cuda.synchronize()
+    assert abs(loss_host.item() - loss) <= 1e-12 * loss
+    assert np.all(np.abs(grad_host.numpy() - g_dev) <= np.maximum(1e-6 * np.abs(g_dev), 1e-12))
     planes, aocc, _ = oracle_scene(sc)
     L_ref = sum(orc.l2_loss_grad(orc.forward(planes, aocc, sc.sh_degree, sc.cameras[v])[0], sc.target(v))[0]
                 for v in st.views)

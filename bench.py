@@ -439,7 +439,7 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": renders_per_step / (float(te.item()) / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(grad_host.nbytes + loss_host.nbytes),
-               "api": "puv_train_step_host (C ABI, host buffers)"}
+               "api": "puv_train_step_host_atlas (C ABI, host buffers)" if cfg != 4 and world == 1 else "puv_train_step_host (C ABI, host buffers)"}
 
     # ---- per-view counts of the last render call on the state (deterministic; read after timing) ----
     st = stepper.st

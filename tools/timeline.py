@@ -15,13 +15,15 @@ from paper_2602_23040_b200.shard import ShardedStep  # noqa: E402
 from synth.scenes import make_scene  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+every = int(sys.argv[2]) if len(sys.argv) > 2 else 1   # views v with v % every == 0 (one rank of `every`)
 sc = make_scene(cfg)
+sc.cameras = [c for v, c in enumerate(sc.cameras) if v % every == 0]
 dev = torch.device("cuda")
 layout = puv.layout_for_levels([(lv.rows, lv.cols) for lv in sc.levels], sc.sh_degree)
 atlas, occ = puv.pack_atlas(layout, [torch.from_numpy(lv.planes).to(dev) for lv in sc.levels],
                             [torch.from_numpy(lv.occ).to(dev) for lv in sc.levels])
 st = ShardedStep(layout, sc.cameras, device=dev)
-tg = torch.from_numpy(np.stack([sc.target(v) for v in st.views])).to(dev)
+tg = torch.from_numpy(np.stack([sc.target(v * every) for v in st.views])).to(dev)
 grad = torch.empty_like(atlas)
 for w in range(3):
     st.step(atlas, occ, tg, grad, check_overflow=(w == 0))

@@ -23,7 +23,7 @@ layout = puv.layout_for_levels([(lv.rows, lv.cols) for lv in sc.levels], sc.sh_d
 atlas, occ = puv.pack_atlas(layout, [torch.from_numpy(lv.planes).to(dev) for lv in sc.levels],
                             [torch.from_numpy(lv.occ).to(dev) for lv in sc.levels])
 st = ShardedStep(layout, sc.cameras, device=dev)
-tg = torch.from_numpy(np.stack([sc.target(v * every) for v in st.views])).to(dev)
+tg = torch.from_numpy(np.stack([sc.target(v) for v in st.views])).to(dev)
 grad = torch.empty_like(atlas)
 for w in range(3):
     st.step(atlas, occ, tg, grad, check_overflow=(w == 0))

@@ -15,6 +15,21 @@
 
 namespace puv {
 
+#ifndef PUV_PBWD_PREFETCH
+#define PUV_PBWD_PREFETCH 1
+#endif
+
+// cp.async (global -> shared, asynchronous, per thread): the next view's depth key and 9 moments
+// are in flight while the current view's chain rule runs, without registers to hold them.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
 template <int DEG, bool LPO>
 #ifndef PUV_PBWD_MINB
 #define PUV_PBWD_MINB 1
@@ -46,13 +61,41 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
 #pragma unroll
   for (int k = 0; k < 3 * NK; ++k) dsh[k] = 0.0;
 
+#if PUV_PBWD_PREFETCH
+  // double-buffered per-thread staging of (depth key, 9 moments) of view i + 1 while view i runs
+  __shared__ double sG2[2][9][128];
+  __shared__ uint32_t sDep[2][128];
+  const int tid = threadIdx.x;
+  auto prefetch = [&](int i, int buf) {
+    if (i < cb.n) {
+      const size_t o = (size_t)(cb.v0 + i) * N + g;
+      cp_async4(&sDep[buf][tid], v.depth + o);
+      const double* src = v.grad2d + 9 * o;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) cp_async8(&sG2[buf][k][tid], src + k);
+    }
+    cp_async_commit();
+  };
+  prefetch(0, 0);
+#endif
   for (int i = 0; i < cb.n; ++i) {
     const size_t o = (size_t)(cb.v0 + i) * N + g;
+#if PUV_PBWD_PREFETCH
+    prefetch(i + 1, (i + 1) & 1);
+    cp_async_wait1();   // view i's group has landed (only view i + 1's may be pending)
+    const int buf = i & 1;
+    if (sDep[buf][tid] == kInvisible) continue;
+    // K6's raw moments (Mx, My, Mxx, Mxy, Myy, dL/do, dL/drgb): see k_raster_bwd.cu
+    const double Mx = sG2[buf][0][tid], My = sG2[buf][1][tid], Mxx = sG2[buf][2][tid], Mxy = sG2[buf][3][tid],
+                 Myy = sG2[buf][4][tid], dO = sG2[buf][5][tid];
+    const double dr = sG2[buf][6][tid], dg = sG2[buf][7][tid], db_ = sG2[buf][8][tid];
+#else
     if (v.depth[o] == kInvisible) continue;
     // K6's raw moments (Mx, My, Mxx, Mxy, Myy, dL/do, dL/drgb): see k_raster_bwd.cu
     const double* g2 = v.grad2d + 9 * o;
     const double Mx = g2[0], My = g2[1], Mxx = g2[2], Mxy = g2[3], Myy = g2[4], dO = g2[5];
     const double dr = g2[6], dg = g2[7], db_ = g2[8];
+#endif
     if (Mx == 0 && My == 0 && Mxx == 0 && Mxy == 0 && Myy == 0 && dO == 0 && dr == 0 && dg == 0 && db_ == 0)
       continue;
     const CamDev& c = cb.c[i];

@@ -14,6 +14,6 @@ for r in $(seq ${ROUNDS:-2}); do
   for v in $VARIANTS; do
     name=${v%%:*}
     PUV_LIB=/tmp/ab_$name.so timeout 600 python bench.py --no-e2e --no-cpu-baseline --no-serial ${BENCH_ARGS:-} > /tmp/ab_out.json 2>/tmp/ab_err.txt
-    python -c "import json,sys; d=json.loads(open('/tmp/ab_out.json').read().strip().splitlines()[-1]); print('$name', round(d['ms_per_step'],2), {k: v for k, v in d['stage_ms_per_step'].items() if k in ('raster_fwd','raster_bwd','project')})" | tee -a gpurun_out/ab.log
+    python -c "import json,sys; d=json.loads(open('/tmp/ab_out.json').read().strip().splitlines()[-1]); print('$name', round(d['ms_per_step'],2), {k: v for k, v in d['stage_ms_per_step'].items() if k in ('raster_fwd','raster_bwd','project','project_bwd')})" | tee -a gpurun_out/ab.log
   done
 done

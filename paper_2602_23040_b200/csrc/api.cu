@@ -703,7 +703,7 @@ static puv_status grad_table(const puv_layout* layout, float* const* atlas_grad,
 // K7 over all views of the call, in camera batches (rows a8, a9)
 static void project_backward(const Common& c, const uint8_t* atlas_occ, int n_views, const puv_camera* cams,
                              const uint8_t* dynamic_mask, const GradTab& G, cudaStream_t s,
-                             const TexelPipe* tout = nullptr) {
+                             const TexelPipe* tout = nullptr, bool overwrite = false) {
   const int nchunk = tout ? tout->n : 1;
   for (int k = 0; k < nchunk; ++k) {
     const int g0 = tout ? tout->bound[k] : 0, g1 = tout ? tout->bound[k + 1] : -1;
@@ -713,7 +713,8 @@ static void project_backward(const Common& c, const uint8_t* atlas_occ, int n_vi
       cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
       for (int i = 0; i < cb.n; ++i) cb.c[i] = cam_dev(cams[v0 + i]);
       StageScope sc(PUV_STAGE_PROJECT_BWD, s);
-      launch_project_bwd(c.plan, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s, g0, g1);
+      // with `overwrite`, the first camera batch writes every texel of the range, the later ones add
+      launch_project_bwd(c.plan, c.views, c.P, atlas_occ, dynamic_mask, cb, G, s, g0, g1, overwrite && v0 == 0);
     }
     if (tout && tout->done[k]) cudaEventRecord(tout->done[k], s);
   }
@@ -787,8 +788,7 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
   if (validate_only) return PUV_OK;
   const float bg[3] = {opts ? opts->bg[0] : 0.f, opts ? opts->bg[1] : 0.f, opts ? opts->bg[2] : 0.f};
   const size_t NA = (size_t)layout->atlas_w * layout->atlas_h, HW3 = (size_t)3 * c.W * c.H;
-  for (int d = 0; d < layout->planes; ++d)
-    if (G.p[d]) cudaMemsetAsync(G.p[d], 0, NA * sizeof(float), s);   // OVERWRITTEN: zero, then accumulate
+  (void)NA;   // OVERWRITTEN: the first chunk's K7 writes every texel (zeros where no gradient), the rest add
   cudaMemsetAsync(b->loss, 0, sizeof(double), s);
   cudaMemsetAsync(b->overflow, 0, sizeof(uint32_t), s);
   cudaMemsetAsync(b->arena_need, 0, sizeof(uint64_t), s);
@@ -806,7 +806,7 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
     launch_overflow_acc(b->state, b->overflow, b->arena_need, s);
     { StageScope sc(PUV_STAGE_RASTER_BWD, s);
       launch_raster_bwd(cc.plan, cc.views, (const uint32_t*)b->arena, b->dL_dimages, 0, n, s); }
-    project_backward(cc, atlas_occ, n, cams + v0, dynamic_mask, G, s, v0 + n >= n_views ? tout : nullptr);
+    project_backward(cc, atlas_occ, n, cams + v0, dynamic_mask, G, s, v0 + n >= n_views ? tout : nullptr, v0 == 0);
   }
   return PUV_OK;
 }

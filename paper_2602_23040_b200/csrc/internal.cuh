@@ -164,7 +164,8 @@ void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, flo
 void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int view0,
                        int n_views, cudaStream_t s);
 void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const uint8_t* mask,
-                        const CamBatch& cb, const GradTab& G, cudaStream_t s, int g0 = 0, int g1 = -1);
+                        const CamBatch& cb, const GradTab& G, cudaStream_t s, int g0 = 0, int g1 = -1,
+                        bool overwrite = false);
 void launch_l2_loss(int64_t n, const float* img, const float* tgt, float* dl, double* loss, cudaStream_t s,
                     bool accumulate);
 void launch_pack(const puv_layout& L, const float* const* level_planes, const uint8_t* const* level_occ,

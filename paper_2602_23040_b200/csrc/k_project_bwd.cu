@@ -37,14 +37,26 @@ template <int DEG, bool LPO>
 __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ,
                                                     const uint8_t* __restrict__ mask, int N,
                                                     const __grid_constant__ CamBatch cb, Views v, GradTab Gt,
-                                                    int g0, int g1) {
+                                                    int g0, int g1, int overwrite) {
   const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;   // texels [g0, g1) of the N
   if (g >= g1) return;
-  if (occ != nullptr && occ[g] == 0) return;
   constexpr int NK = (DEG + 1) * (DEG + 1);
+  // overwrite: the first K7 of a train step WRITES the texel's gradient (zeros where it has none),
+  // so the step needs neither a memset of the planes nor a read-modify-write
+  auto put = [&](int d, float x) {
+    if (overwrite) Gt.p[d][g] = x;
+    else Gt.p[d][g] += x;
+  };
+  auto zero_all = [&]() {
+    if (!overwrite) return;
+#pragma unroll
+    for (int d = 0; d < 11 + 3 * NK; ++d)
+      if (Gt.p[d]) Gt.p[d][g] = 0.0f;
+  };
+  if (occ != nullptr && occ[g] == 0) { zero_all(); return; }
   bool any = false;
   for (int i = 0; i < cb.n; ++i) any |= v.depth[(size_t)(cb.v0 + i) * N + g] != kInvisible;
-  if (!any) return;
+  if (!any) { zero_all(); return; }
 
   float fmx, fmy, fmz;
   texel_mu<LPO>(P, pm, g, fmx, fmy, fmz);   // the fp32 position the render saw (xyz or c (+) rho (x) ray)
@@ -205,34 +217,34 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
   const double dqy = 2 * (-2 * y * dR00 + x * dR01 + w * dR02 + x * dR10 + z * dR12 - w * dR20 + z * dR21 - 2 * y * dR22);
   const double dqz = 2 * (-2 * z * dR00 - w * dR01 + x * dR02 + w * dR10 - 2 * z * dR11 + y * dR12 + x * dR20 + y * dR21);
   const double qd = w * dqw + x * dqx + y * dqy + z * dqz;
-  if (mask != nullptr && mask[g] == 0) return;   // gradient freezing: D_i = 0
+  if (mask != nullptr && mask[g] == 0) { zero_all(); return; }   // gradient freezing: D_i = 0
   if (pm.rho) {   // d rho = ray . d mu, in fp64 before the one rounding (planes 1, 2 untouched)
-    Gt.p[0][g] += (float)((double)__ldg(P.p[pm.D] + g) * dmu0 + (double)__ldg(P.p[pm.D + 1] + g) * dmu1 +
-                          (double)__ldg(P.p[pm.D + 2] + g) * dmu2);
+    put(0, (float)((double)__ldg(P.p[pm.D] + g) * dmu0 + (double)__ldg(P.p[pm.D + 1] + g) * dmu1 +
+                          (double)__ldg(P.p[pm.D + 2] + g) * dmu2));
   } else {
-    Gt.p[0][g] += (float)dmu0;
-    Gt.p[1][g] += (float)dmu1;
-    Gt.p[2][g] += (float)dmu2;
+    put(0, (float)dmu0);
+    put(1, (float)dmu1);
+    put(2, (float)dmu2);
   }
-  Gt.p[3][g] += (float)(2 * t0 * dt0);
-  Gt.p[4][g] += (float)(2 * t1 * dt1);
-  Gt.p[5][g] += (float)(2 * t2 * dt2);
-  Gt.p[6][g] += (float)((dqw - w * qd) * iq);
-  Gt.p[7][g] += (float)((dqx - x * qd) * iq);
-  Gt.p[8][g] += (float)((dqy - y * qd) * iq);
-  Gt.p[9][g] += (float)((dqz - z * qd) * iq);
-  Gt.p[10][g] += (float)(dop * u.o * (1.0 - u.o));
+  put(3, (float)(2 * t0 * dt0));
+  put(4, (float)(2 * t1 * dt1));
+  put(5, (float)(2 * t2 * dt2));
+  put(6, (float)((dqw - w * qd) * iq));
+  put(7, (float)((dqx - x * qd) * iq));
+  put(8, (float)((dqy - y * qd) * iq));
+  put(9, (float)((dqz - z * qd) * iq));
+  put(10, (float)(dop * u.o * (1.0 - u.o)));
 #pragma unroll
-  for (int k = 0; k < 3 * NK; ++k) Gt.p[11 + k][g] += (float)dsh[k];
+  for (int k = 0; k < 3 * NK; ++k) put(11 + k, (float)dsh[k]);
 }
 
 void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const uint8_t* mask,
-                        const CamBatch& cb, const GradTab& G, cudaStream_t s, int g0, int g1) {
+                        const CamBatch& cb, const GradTab& G, cudaStream_t s, int g0, int g1, bool overwrite) {
   if (g1 < 0) g1 = p.N;
   if (g1 <= g0) return;
   const int threads = 128;
   const int blocks = (g1 - g0 + threads - 1) / threads;
-#define PUV_K7(D, L) k_project_bwd<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G, g0, g1)
+#define PUV_K7(D, L) k_project_bwd<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G, g0, g1, overwrite ? 1 : 0)
   const bool lpo = P.qspec != nullptr;
   switch (p.deg) {
     case 0: if (lpo) PUV_K7(0, true); else PUV_K7(0, false); break;

@@ -30,8 +30,22 @@ constexpr float kLog2e = 1.44269504f;
 // exp_c (R13): Cody-Waite reduction by ln2 (hi/lo) + degree-7 Taylor, Horner with fma.
 // exp_c_core is exp_c without the range clamps, for callers whose argument is known to lie in (-87, 88) (the
 // compositing range: power in [t_g, 0] with t_g = -log_c(255 o) >= -5.55): bit-identical there.
+#ifndef PUV_EXPC_MAGIC
+#define PUV_EXPC_MAGIC 1
+#endif
 PUV_DEV float exp_c_core(float x) {
+#if PUV_EXPC_MAGIC
+  // rint by the 1.5 * 2^23 shifter: for |v| < 2^22 the RN addition rounds v to the nearest integer
+  // (ties to even), exactly rintf(v), and the sum's low mantissa bits are that integer -- one FADD
+  // pair instead of FRND + F2I (conversion-pipe ops); bit-identical to the rintf form
+  constexpr float kShifter = 12582912.0f;   // 1.5 * 2^23
+  const float t = add(mul(x, kLog2e), kShifter);
+  const float k = sub(t, kShifter);
+  const int ki = __float_as_int(t) - 0x4b400000;
+#else
   const float k = rintf(mul(x, kLog2e));
+  const int ki = (int)k;
+#endif
   float r = fma_(-k, kLn2Hi, x);
   r = fma_(-k, kLn2Lo, r);
   float p = (float)(1.0 / 5040.0);
@@ -42,7 +56,7 @@ PUV_DEV float exp_c_core(float x) {
   p = fma_(p, r, 0.5f);
   p = fma_(p, r, 1.0f);
   p = fma_(p, r, 1.0f);
-  const float two_k = __int_as_float(((int)k + 127) << 23);
+  const float two_k = __int_as_float((ki + 127) << 23);
   return mul(p, two_k);
 }
 

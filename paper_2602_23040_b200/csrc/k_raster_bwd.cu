@@ -55,6 +55,9 @@ constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4
 #ifndef PUV_BWD_BATCH
 #define PUV_BWD_BATCH 64
 #endif
+#ifndef PUV_BWD_KSKIP
+#define PUV_BWD_KSKIP 1
+#endif
 constexpr int kBwdBatch = PUV_BWD_BATCH;                   // entries staged per batch
 
 // Alternative reduction (-DPUV_BWD_SMEM_RED).  Sum the 9 per-lane values x[0..8] over the warp
@@ -269,6 +272,9 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       const bool may_cap = !(B.z < 0.99f);
       bool act[kBwdPPT], cap[kBwdPPT];
       bool any = false;
+      // kact[k] (warp-uniform): some lane's pixel k (the warp's 8x4 sub-block k) may composite the
+      // entry; a sub-block with none skips its body (PUV_BWD_KSKIP)
+      bool kact[kBwdPPT];
       if (e < (uint32_t)kMaskCap) {
         static_assert(kBwdPPT == 4, "the K5 mask layout assumes 4 pixels per K6 thread");
         const uint4 mw = sM[j][warp];
@@ -276,6 +282,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
 #pragma unroll
         for (int k = 0; k < kBwdPPT; ++k) {
           act[k] = e < last[k] && ((words[k] >> lane) & 1u);
+          kact[k] = words[k] != 0u;   // a superset of the lanes' act (stale bits past last only add)
           any |= act[k];
         }
       } else {
@@ -284,6 +291,7 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
         for (int k = 0; k < kBwdPPT; ++k) {
           const float power = pair_power(A.x, A.y, A.z, A.w, B.x, fi[k], fj[k]);
           act[k] = e < last[k] && !(power > 0.0f || power < B.y);
+          kact[k] = __any_sync(0xffffffffu, act[k]);
           any |= act[k];
         }
       }
@@ -313,6 +321,9 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
         constexpr bool kCap = decltype(cap_tag)::value;
 #pragma unroll
         for (int k = 0; k < kBwdPPT; ++k) {
+#if PUV_BWD_KSKIP
+          if (!kact[k]) continue;   // warp-uniform: no pixel of sub-block k composites this entry
+#endif
           const double dy = d0.y - dj[k];
 #if PUV_BWD_EXPSEL
           // an inactive pixel gets G = e^-700 (~1e-304): its alpha, moments and colour terms vanish

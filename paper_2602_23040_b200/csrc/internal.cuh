@@ -6,6 +6,10 @@
 
 #include "../../include/puv.h"
 
+#ifndef PUV_RASTER_CARVEOUT
+#define PUV_RASTER_CARVEOUT -1   // -1: driver default
+#endif
+
 namespace puv {
 
 constexpr int kMaxPlanes = 11 + 3 * 16 + 3;   // SH degree 3 + the 3 ray planes of PUV_POS_RHO

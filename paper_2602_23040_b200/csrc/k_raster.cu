@@ -329,6 +329,13 @@ void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, flo
                        const float bg[3], cudaStream_t s) {
   if (n_views <= 0 || p.ntiles <= 0) return;
   const dim3 grid(p.ntiles, n_views);
+#if PUV_RASTER_CARVEOUT >= 0
+  // shared-memory carveout preference (percent): lets the driver pick a larger carveout so the
+  // register-limited residency is not capped by the shared-memory configuration
+  static const bool carve_once =
+      cudaFuncSetAttribute(k_raster_fwd, cudaFuncAttributePreferredSharedMemoryCarveout, PUV_RASTER_CARVEOUT) == cudaSuccess;
+  (void)carve_once;
+#endif
   k_raster_fwd<<<grid, kRasterThreads, 0, s>>>(arena, v, view0, p.N, p.W, p.H, p.gx, p.ntiles, bg[0], bg[1], bg[2],
                                                images);
   count_launches(1);

@@ -56,7 +56,7 @@ constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4
 #define PUV_BWD_BATCH 64
 #endif
 #ifndef PUV_BWD_KSKIP
-#define PUV_BWD_KSKIP 1
+#define PUV_BWD_KSKIP 0
 #endif
 constexpr int kBwdBatch = PUV_BWD_BATCH;                   // entries staged per batch
 
@@ -387,6 +387,13 @@ void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, con
                        int n_views, cudaStream_t s) {
   if (n_views <= 0 || p.ntiles <= 0) return;
   const dim3 grid(p.ntiles, n_views);
+#if PUV_RASTER_CARVEOUT >= 0
+  // shared-memory carveout preference (percent): lets the driver pick a larger carveout so the
+  // register-limited residency is not capped by the shared-memory configuration
+  static const bool carve_once =
+      cudaFuncSetAttribute(k_raster_bwd, cudaFuncAttributePreferredSharedMemoryCarveout, PUV_RASTER_CARVEOUT) == cudaSuccess;
+  (void)carve_once;
+#endif
   k_raster_bwd<<<grid, kBwdThreads, 0, s>>>(arena, v, p.N, p.W, p.H, p.gx, p.ntiles, view0, dL_dimages);
   count_launches(1);
 }

@@ -370,8 +370,9 @@ typedef struct {
   const float* t_final;          /* device, H*W: fp32 contract transmittance after the last entry */
   const uint32_t* n_contrib;     /* device, H*W: list position after the last composited entry */
   const double* grad2d;          /* device, H_A*W_A*9 fp64, per Gaussian, of the last backward: pixel moments
-                                    (Mx,My,Mxx,Mxy,Myy) of G dL/dalpha, dL/do, dL/d(r,g,b); dL/d(mx,my,ha,nb,hc) =
-                                    o (2ha Mx + nb My, nb Mx + 2hc My, Mxx, Mxy, Myy) (k_raster_bwd.cu) */
+                                    (Mx,My,Mxx,Mxy,Myy) of alpha dL/dalpha (= o G dL/dalpha), o dL/do, dL/d(r,g,b);
+                                    dL/d(mx,my,ha,nb,hc) = (2ha Mx + nb My, nb Mx + 2hc My, Mxx, Mxy, Myy)
+                                    (k_raster_bwd.cu; a -DPUV_LNO=0 build stores the moments of G dL/dalpha) */
   const uint32_t* depth_order;   /* device, n_visible gids sorted by (depth_bits, gid) */
   uint64_t n_examined;           /* (pixel, entry) pairs that ran the skip test in the forward */
   uint64_t n_composited;         /* pairs composited in the forward */

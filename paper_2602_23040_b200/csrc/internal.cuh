@@ -6,6 +6,14 @@
 
 #include "../../include/puv.h"
 
+// PUV_LNO: the fp64 value record carries ln(o) instead of o, folded into the Gaussian exponent
+// (alpha = exp(power + ln o): one DMUL less per composited pixel in K5 and K6); K6's moments are
+// then o-scaled (sums of alpha dL/dalpha) and K7 drops its o factors
+#ifndef PUV_LNO
+#define PUV_LNO 1
+#endif
+constexpr bool kLno = PUV_LNO != 0;
+
 #ifndef PUV_RASTER_CARVEOUT
 #define PUV_RASTER_CARVEOUT -1   // -1: driver default
 #endif
@@ -116,7 +124,7 @@ struct Plan {
 
 // Records of a visible (view, Gaussian):
 //  rec   (fp32 contract, 32 B): A=(mx,my,ha,nb) B=(hc,t_g,o,flags)  -> every decision; flags = SH clamp bits (K7)
-//  rec64 (fp64 values,   80 B): (mx,my) (ha,nb) (hc,o) (r,g) (b,-)               -> backward values
+//  rec64 (fp64 values,   80 B): (mx,my) (ha,nb) (hc,ln o) (r,g) (b,-)   (o itself when !kLno)               -> backward values
 struct Views {
   uint32_t* depth;   // [V][N]
   uint2* rect;       // [V][N]  (x0 | x1<<16, y0 | y1<<16)

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
   const Unpacked u = unpack_contract(ls0, ls1, ls2, qw, qx, qy, qz, logit);
   bool any = false;
   Unpacked64 u64;
+  double lno = 0.0;   // ln o = -log1p(e^-logit), once per texel (kLno)
   float sh[3 * NK];
 
   for (int i = 0; i < cb.n; ++i) {
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
     if (!any) {  // first visible view of this texel: fp64 unpack + SH coefficients
       any = true;
       u64 = unpack64(ls0, ls1, ls2, qw, qx, qy, qz, logit);
+      if (kLno) lno = -log1p(exp(-(double)logit));
 #pragma unroll
       for (int k = 0; k < 3 * NK; ++k) sh[k] = plane_value<LPO>(P, 11 + k, g);
     }
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
     double2* r64 = v.rec64 + 5 * o;
     r64[0] = make_double2(p64.mx, p64.my);
     r64[1] = make_double2(p64.ha, p64.nb);
-    r64[2] = make_double2(p64.hc, u64.o);
+    r64[2] = make_double2(p64.hc, kLno ? lno : u64.o);
     r64[3] = make_double2(rgb[0], rgb[1]);
     r64[4] = make_double2(rgb[2], 0.0);
   }

@@ -116,8 +116,10 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
     const double a = p.a, b = p.b, cc = p.c, id2 = 1.0 / (p.det * p.det);
     // power = ha dx^2 + nb dx dy + hc dy^2 with (ha, nb, hc) = (-c/2, b, -a/2) / det, alpha = o e^power
     const double idet = 1.0 / p.det, ha = -0.5 * cc * idet, nb = b * idet, hc = -0.5 * a * idet;
-    const double dmx = u.o * (2.0 * ha * Mx + nb * My), dmy = u.o * (nb * Mx + 2.0 * hc * My);
-    const double dha = u.o * Mxx, dnb = u.o * Mxy, dhc = u.o * Myy;
+    // kLno: K6's moments are already o-scaled (sums of alpha dL/dalpha = o G dL/dalpha)
+    const double os = kLno ? 1.0 : u.o;
+    const double dmx = os * (2.0 * ha * Mx + nb * My), dmy = os * (nb * Mx + 2.0 * hc * My);
+    const double dha = os * Mxx, dnb = os * Mxy, dhc = os * Myy;
     // conic (ha, nb, hc) = (-c/2, b, -a/2) / det
     const double da = (dha * 0.5 * cc * cc - dnb * b * cc + dhc * 0.5 * b * b) * id2;
     const double db = (-dha * b * cc + dnb * (a * cc + b * b) - dhc * a * b) * id2;
@@ -233,7 +235,8 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
   put(7, (float)((dqx - x * qd) * iq));
   put(8, (float)((dqy - y * qd) * iq));
   put(9, (float)((dqz - z * qd) * iq));
-  put(10, (float)(dop * u.o * (1.0 - u.o)));
+  // dL/dlogit = dL/do o (1 - o); with kLno dop already sums o dL/do
+  put(10, (float)(dop * (kLno ? 1.0 : u.o) * (1.0 - u.o)));
 #pragma unroll
   for (int k = 0; k < 3 * NK; ++k) put(11 + k, (float)dsh[k]);
 }

@@ -215,7 +215,8 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
       const double2 d0 = sD[0][j], d1 = sD[1][j], d2 = sD[2][j], d3 = sD[3][j];
       const double d4x = sD[4][j].x;
       const double dx = d0.x - di;
-      const double hadxx = d1.x * (dx * dx), nbdx = d1.y * dx;
+      // kLno: ln o rides in the column term, so exp64(power64) is alpha itself
+      const double hadxx = kLno ? fma(d1.x, dx * dx, d2.y) : d1.x * (dx * dx), nbdx = d1.y * dx;
 #if PUV_FWD_BRANCHFREE
       // both pixels' bodies run under selects (no divergent branches): the contract on a safe
       // argument (power 0) where the pixel did not hit, every state update gated by its flags
@@ -233,7 +234,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
         last[k] = comp[k] ? e + 1 : last[k];
         n_comp += comp[k] ? 1u : 0u;
         const double pw = power64(d2.x, hadxx, nbdx, d0.y - dj[k]);
-        const double a64 = capped ? 0.99 : d2.y * exp64(fmax(pw, -700.0), sExp);
+        const double a64 = capped ? 0.99 : (kLno ? 1.0 : d2.y) * exp64(fmax(pw, -700.0), sExp);
         const double w = comp[k] ? a64 * T64[k] : 0.0;
         C[k][0] = fma(d3.x, w, C[k][0]);
         C[k][1] = fma(d3.y, w, C[k][1]);
@@ -261,7 +262,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
 #endif
         // fp64 value of the composited pair
         const double pw = power64(d2.x, hadxx, nbdx, d0.y - dj[k]);
-        const double a64 = capped ? 0.99 : d2.y * exp64(pw, sExp);
+        const double a64 = capped ? 0.99 : (kLno ? exp64(pw, sExp) : d2.y * exp64(pw, sExp));
         const double w = a64 * T64[k];
         C[k][0] = fma(d3.x, w, C[k][0]);
         C[k][1] = fma(d3.y, w, C[k][1]);

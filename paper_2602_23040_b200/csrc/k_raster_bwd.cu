@@ -16,7 +16,9 @@
 //   dL/dmx = o (2 ha Mx + nb My), dL/dmy = o (nb Mx + 2 hc My), dL/d(ha, nb, hc) = o (Mxx, Mxy, Myy)
 //   Mx = sum GdL dx, My = sum GdL dy, Mxx = sum GdL dx^2, Mxy = sum GdL dx dy, Myy = sum GdL dy^2.
 // K6 accumulates the raw moments (Mx, My, Mxx, Mxy, Myy, sum GdL, dL/dc) per (view, Gaussian);
-// K7 applies the (linear) o-scaling and the conic mixing once per (view, Gaussian).
+// K7 applies the (linear) o-scaling and the conic mixing once per (view, Gaussian).  With kLno
+// (default) the record holds ln o, exp64 returns alpha = o G directly and the moments are taken of
+// o GdL (the o-scaling is already in; sum o GdL = o dL/do), so K7 only mixes.
 // The per-pixel body is branch-free (inactive pixels get a = 0 and masked terms), so the
 // pixels' fp64 chains interleave.  A thread sums the 9 moments of an entry over its pixels; the
 // warp sums them with a transposing shuffle butterfly and 9 lanes issue one fp64 atomic
@@ -33,7 +35,7 @@ namespace puv {
 #define PUV_BWD_PPT 4
 #endif
 #ifndef PUV_BWD_MINB
-#define PUV_BWD_MINB 8
+#define PUV_BWD_MINB 10
 #endif
 #if PUV_BWD_MINB > 0
 #define PUV_BWD_BOUNDS __launch_bounds__(kTile * kTile / PUV_BWD_PPT, PUV_BWD_MINB)
@@ -312,7 +314,8 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       // the thread's pixels share the column px: dx and its terms are computed once, and the
       // dx-only moments follow from the thread's sum of GdL (Mx = dx S, Mxx = dx^2 S)
       const double dx = d0.x - di, dxx = dx * dx;
-      const double hadxx = d1.x * dxx, nbdx = d1.y * dx;
+      // kLno: ln o rides in the column term: exp64(power64) = alpha = o G, and GdL below is o G dL/da
+      const double hadxx = kLno ? fma(d1.x, dxx, d2.y) : d1.x * dxx, nbdx = d1.y * dx;
       double gv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // Mx, My, Mxx, Mxy, Myy, sum GdL, colour r, g, b
       double sdy = 0.0;                              // sum GdL dy (-> Mxy = dx sdy)
       // The pixel bodies, compiled twice: the alpha-cap selects exist only in the (warp-uniform,
@@ -330,10 +333,10 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
           // below any nonzero fp64 sum, so the two result selects become one argument select
           const double pw = power64(d2.x, hadxx, nbdx, dy);
           const double G = exp64(act[k] ? pw : -700.0, sExp);
-          double a = o * G;
+          double a = kLno ? G : o * G;
 #else
           const double G = exp64(power64(d2.x, hadxx, nbdx, dy), sExp);
-          double a = act[k] ? o * G : 0.0;
+          double a = act[k] ? (kLno ? G : o * G) : 0.0;
 #endif
           if (kCap) a = cap[k] ? 0.99 : a;
           const double aT = a * T[k];

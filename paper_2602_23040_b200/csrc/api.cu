@@ -799,13 +799,17 @@ static puv_status train_step_enqueue(const puv_layout* layout, const float* cons
     cc.views = views_of(cc.plan, b->state);
     // each view's loss gradient on the second stream as soon as it is composited, and the zeroing
     // of K6's moment slots there too: both overlap the compositing of later views
-    const L2Hook hook{targets + (size_t)v0 * HW3, b->dL_dimages, b->loss, v0 == 0 ? targets_ready : nullptr, false,
-                      cc.views.grad2d, (size_t)72 * n * cc.plan.N};
+    // kStepOverlap: each view's composite backward also runs on the second stream right after its
+    // loss gradient (beside the compositing of later views); else one K6 launch for the chunk
+    const L2Hook hook{targets + (size_t)v0 * HW3, b->dL_dimages, b->loss, v0 == 0 ? targets_ready : nullptr,
+                      kStepOverlap, cc.views.grad2d, (size_t)72 * n * cc.plan.N};
     render_pipeline(cc, atlas_occ, n, cams + v0, bg, b->images, b->state, b->arena, b->arena_bytes, s, &hook,
                     v0 == 0 ? tin : nullptr);
     launch_overflow_acc(b->state, b->overflow, b->arena_need, s);
-    { StageScope sc(PUV_STAGE_RASTER_BWD, s);
-      launch_raster_bwd(cc.plan, cc.views, (const uint32_t*)b->arena, b->dL_dimages, 0, n, s); }
+    if (!kStepOverlap) {
+      StageScope sc(PUV_STAGE_RASTER_BWD, s);
+      launch_raster_bwd(cc.plan, cc.views, (const uint32_t*)b->arena, b->dL_dimages, 0, n, s);
+    }
     project_backward(cc, atlas_occ, n, cams + v0, dynamic_mask, G, s, v0 + n >= n_views ? tout : nullptr, v0 == 0);
   }
   return PUV_OK;

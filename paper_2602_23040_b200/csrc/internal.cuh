@@ -14,6 +14,11 @@
 #endif
 constexpr bool kLno = PUV_LNO != 0;
 
+#ifndef PUV_STEP_OVERLAP
+#define PUV_STEP_OVERLAP 0
+#endif
+constexpr bool kStepOverlap = PUV_STEP_OVERLAP != 0;   // train step: per-view K6 beside later K5s
+
 #ifndef PUV_RASTER_CARVEOUT
 #define PUV_RASTER_CARVEOUT -1   // -1: driver default
 #endif

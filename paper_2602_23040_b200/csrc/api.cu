@@ -201,6 +201,10 @@ static CamDev cam_dev(const puv_camera& c) {
   // R5: lim = 1.3 * tan(fov/2) = 1.3 * 0.5 * W / fx in fp64, rounded to fp32
   d.limx = (float)(1.3 * 0.5 * (double)c.width / (double)c.fx);
   d.limy = (float)(1.3 * 0.5 * (double)c.height / (double)c.fy);
+  for (int k = 0; k < 12; ++k) d.V64[k] = d.V[k];
+  d.fx64 = d.fx; d.fy64 = d.fy; d.cx64 = d.cx; d.cy64 = d.cy;
+  d.limx64 = d.limx; d.limy64 = d.limy;
+  for (int k = 0; k < 3; ++k) d.campos64[k] = d.campos[k];
   return d;
 }
 

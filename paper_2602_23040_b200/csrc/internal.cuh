@@ -80,6 +80,10 @@ struct CamDev {
   float near_plane;
   float campos[3];
   float limx, limy;
+  // the same values widened on the host (exact): the fp64 value path reads these instead of
+  // converting the fp32 fields per (view, texel) (F2F is a quarter-rate conversion op)
+  double V64[12];
+  double fx64, fy64, cx64, cy64, limx64, limy64, campos64[3];
 };
 struct CamBatch { CamDev c[kCamBatch]; int n; int v0; };
 

@@ -12,6 +12,9 @@
 namespace puv {
 
 template <int DEG, bool LPO>
+#ifndef PUV_PROJ_SH_SMEM
+#define PUV_PROJ_SH_SMEM 1
+#endif
 #ifndef PUV_PROJ_MINB
 #define PUV_PROJ_MINB 3
 #endif
@@ -32,7 +35,15 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
   bool any = false;
   Unpacked64 u64;
   double lno = 0.0;   // ln o = -log1p(e^-logit), once per texel (kLno)
+#if PUV_PROJ_SH_SMEM
+  // the texel's SH coefficients widened to fp64 once (not per view): [3 NK][128] doubles
+  __shared__ double sSH[3 * NK][128];
+  const int tid = threadIdx.x;
+#define PUV_SH(k) sSH[k][tid]
+#else
   float sh[3 * NK];
+#define PUV_SH(k) ((double)sh[k])
+#endif
 
   for (int i = 0; i < cb.n; ++i) {
     const CamDev& c = cb.c[i];
@@ -53,11 +64,15 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
       u64 = unpack64(ls0, ls1, ls2, qw, qx, qy, qz, logit);
       if (kLno) lno = -log1p(exp(-(double)logit));
 #pragma unroll
+#if PUV_PROJ_SH_SMEM
+      for (int k = 0; k < 3 * NK; ++k) sSH[k][tid] = plane_value<LPO>(P, 11 + k, g);
+#else
       for (int k = 0; k < 3 * NK; ++k) sh[k] = plane_value<LPO>(P, 11 + k, g);
+#endif
     }
     const Proj64 p64 = project64(c, mux, muy, muz, u64, cp.clx, cp.cly);
     // SH colour (R3) in fp64; the clamp decision is recorded for K7
-    double dx = (double)mux - c.campos[0], dy = (double)muy - c.campos[1], dz = (double)muz - c.campos[2];
+    double dx = (double)mux - c.campos64[0], dy = (double)muy - c.campos64[1], dz = (double)muz - c.campos64[2];
     const double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
     dx *= inv; dy *= inv; dz *= inv;
     double Y[NK];
@@ -67,7 +82,7 @@ __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosM
     for (int ch = 0; ch < 3; ++ch) {
       double acc = 0.5;
 #pragma unroll
-      for (int k = 0; k < NK; ++k) acc = fma(Y[k], (double)sh[3 * k + ch], acc);
+      for (int k = 0; k < NK; ++k) acc = fma(Y[k], PUV_SH(3 * k + ch), acc);
       rgb[ch] = acc;
     }
     uint32_t flags = 0;

@@ -30,6 +30,9 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+#ifndef PUV_PBWD_SH_SMEM
+#define PUV_PBWD_SH_SMEM 1
+#endif
 template <int DEG, bool LPO>
 #ifndef PUV_PBWD_MINB
 #define PUV_PBWD_MINB 1
@@ -54,6 +57,7 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
       if (Gt.p[d]) Gt.p[d][g] = 0.0f;
   };
   if (occ != nullptr && occ[g] == 0) { zero_all(); return; }
+  if (mask != nullptr && mask[g] == 0) { zero_all(); return; }   // gradient freezing: D_i = 0 (no work)
   bool any = false;
   for (int i = 0; i < cb.n; ++i) any |= v.depth[(size_t)(cb.v0 + i) * N + g] != kInvisible;
   if (!any) { zero_all(); return; }
@@ -69,6 +73,15 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
 
   double dmu0 = 0, dmu1 = 0, dmu2 = 0, dop = 0;
   double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;  // G = dSigma + dSigma^T
+#if PUV_PBWD_SH_SMEM
+  // the texel's SH coefficients k >= 1 widened to fp64 once (dynamic smem [3 (NK - 1)][128]), not
+  // re-read and converted per view
+  extern __shared__ double sSHd[];
+  for (int k = 3; k < 3 * NK; ++k) sSHd[(k - 3) * 128 + threadIdx.x] = plane_value<LPO>(P, 11 + k, g);
+#define PUV_SHW(i) sSHd[((i) - 3) * 128 + threadIdx.x]
+#else
+#define PUV_SHW(i) ((double)plane_value<LPO>(P, 11 + (i), g))
+#endif
   double dsh[3 * NK];
 #pragma unroll
   for (int k = 0; k < 3 * NK; ++k) dsh[k] = 0.0;
@@ -143,12 +156,12 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
     for (int k = 0; k < 3; ++k) {
       const double dT0 = 2 * da * St0[k] + db * St1[k];
       const double dT1 = 2 * dc * St1[k] + db * St0[k];
-      dJ00 += dT0 * (double)c.V[k];
-      dJ02 += dT0 * (double)c.V[8 + k];
-      dJ11 += dT1 * (double)c.V[4 + k];
-      dJ12 += dT1 * (double)c.V[8 + k];
+      dJ00 += dT0 * c.V64[k];
+      dJ02 += dT0 * c.V64[8 + k];
+      dJ11 += dT1 * c.V64[4 + k];
+      dJ12 += dT1 * c.V64[8 + k];
     }
-    const double fx = c.fx, fy = c.fy, iz = 1.0 / p.z, iz2 = iz * iz;
+    const double fx = c.fx64, fy = c.fy64, iz = 1.0 / p.z, iz2 = iz * iz;
     double dpx = 0, dpy = 0, dpz = -(dJ00 * fx + dJ11 * fy) * iz2;
     if (cp.clx == 0) { dpx -= dJ02 * fx * iz2; dpz += 2 * dJ02 * fx * p.x * iz2 * iz; }
     else dpz += dJ02 * fx * p.cxp * iz2;
@@ -158,14 +171,14 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
     dpx += dmx * fx * iz;
     dpy += dmy * fy * iz;
     dpz -= (dmx * fx * p.x + dmy * fy * p.y) * iz2;
-    dmu0 += (double)c.V[0] * dpx + (double)c.V[4] * dpy + (double)c.V[8] * dpz;
-    dmu1 += (double)c.V[1] * dpx + (double)c.V[5] * dpy + (double)c.V[9] * dpz;
-    dmu2 += (double)c.V[2] * dpx + (double)c.V[6] * dpy + (double)c.V[10] * dpz;
+    dmu0 += c.V64[0] * dpx + c.V64[4] * dpy + c.V64[8] * dpz;
+    dmu1 += c.V64[1] * dpx + c.V64[5] * dpy + c.V64[9] * dpz;
+    dmu2 += c.V64[2] * dpx + c.V64[6] * dpy + c.V64[10] * dpz;
     dop += dO;
     // colour
     const uint32_t flags = __float_as_uint(v.rec[2 * o + 1].w);
     const double drgb[3] = {(flags & 1u) ? 0.0 : dr, (flags & 2u) ? 0.0 : dg, (flags & 4u) ? 0.0 : db_};
-    double ex = mux - (double)c.campos[0], ey = muy - (double)c.campos[1], ez = muz - (double)c.campos[2];
+    double ex = mux - c.campos64[0], ey = muy - c.campos64[1], ez = muz - c.campos64[2];
     const double dist = sqrt(ex * ex + ey * ey + ez * ez), idist = 1.0 / dist;
     ex *= idist; ey *= idist; ez *= idist;
     double Y[NK];
@@ -180,8 +193,7 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
       double dd0 = 0, dd1 = 0, dd2 = 0;
 #pragma unroll
       for (int k = 1; k < NK; ++k) {
-        const double w = (double)plane_value<LPO>(P, 11 + 3 * k, g) * drgb[0] +
-                         (double)plane_value<LPO>(P, 12 + 3 * k, g) * drgb[1] + (double)plane_value<LPO>(P, 13 + 3 * k, g) * drgb[2];
+        const double w = PUV_SHW(3 * k) * drgb[0] + PUV_SHW(3 * k + 1) * drgb[1] + PUV_SHW(3 * k + 2) * drgb[2];
         dd0 = fma(w, dY[k][0], dd0);
         dd1 = fma(w, dY[k][1], dd1);
         dd2 = fma(w, dY[k][2], dd2);
@@ -219,7 +231,6 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
   const double dqy = 2 * (-2 * y * dR00 + x * dR01 + w * dR02 + x * dR10 + z * dR12 - w * dR20 + z * dR21 - 2 * y * dR22);
   const double dqz = 2 * (-2 * z * dR00 - w * dR01 + x * dR02 + w * dR10 - 2 * z * dR11 + y * dR12 + x * dR20 + y * dR21);
   const double qd = w * dqw + x * dqx + y * dqy + z * dqz;
-  if (mask != nullptr && mask[g] == 0) { zero_all(); return; }   // gradient freezing: D_i = 0
   if (pm.rho) {   // d rho = ray . d mu, in fp64 before the one rounding (planes 1, 2 untouched)
     put(0, (float)((double)__ldg(P.p[pm.D] + g) * dmu0 + (double)__ldg(P.p[pm.D + 1] + g) * dmu1 +
                           (double)__ldg(P.p[pm.D + 2] + g) * dmu2));
@@ -247,7 +258,20 @@ void launch_project_bwd(const Plan& p, const Views& v, const PlaneTab& P, const 
   if (g1 <= g0) return;
   const int threads = 128;
   const int blocks = (g1 - g0 + threads - 1) / threads;
+#if PUV_PBWD_SH_SMEM
+#define PUV_K7(D, L)                                                                                      \
+  do {                                                                                                    \
+    constexpr int smem = 3 * ((D + 1) * (D + 1) - 1) * 128 * 8;                                           \
+    static const bool attr =                                                                              \
+        cudaFuncSetAttribute(k_project_bwd<D, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==   \
+        cudaSuccess;                                                                                      \
+    (void)attr;                                                                                           \
+    k_project_bwd<D, L><<<blocks, threads, smem, s>>>(P, p.pm, occ, mask, p.N, cb, v, G, g0, g1,          \
+                                                      overwrite ? 1 : 0);                                 \
+  } while (0)
+#else
 #define PUV_K7(D, L) k_project_bwd<D, L><<<blocks, threads, 0, s>>>(P, p.pm, occ, mask, p.N, cb, v, G, g0, g1, overwrite ? 1 : 0)
+#endif
   const bool lpo = P.qspec != nullptr;
   switch (p.deg) {
     case 0: if (lpo) PUV_K7(0, true); else PUV_K7(0, false); break;

@@ -240,20 +240,20 @@ struct Proj64 {
 PUV_DEV Proj64 project64(const CamDev& cam, double mx_, double my_, double mz_, const Unpacked64& u, int clx,
                          int cly) {
   Proj64 p;
-  const float* V = cam.V;
-  p.x = (double)V[0] * mx_ + (double)V[1] * my_ + (double)V[2] * mz_ + (double)V[3];
-  p.y = (double)V[4] * mx_ + (double)V[5] * my_ + (double)V[6] * mz_ + (double)V[7];
-  p.z = (double)V[8] * mx_ + (double)V[9] * my_ + (double)V[10] * mz_ + (double)V[11];
+  const double* V = cam.V64;
+  p.x = V[0] * mx_ + V[1] * my_ + V[2] * mz_ + V[3];
+  p.y = V[4] * mx_ + V[5] * my_ + V[6] * mz_ + V[7];
+  p.z = V[8] * mx_ + V[9] * my_ + V[10] * mz_ + V[11];
   p.ux = p.x / p.z;
   p.uy = p.y / p.z;
-  p.cxp = clx ? clx * (double)cam.limx : p.ux;
-  p.cyp = cly ? cly * (double)cam.limy : p.uy;
-  const double fx = cam.fx, fy = cam.fy;
+  p.cxp = clx ? clx * cam.limx64 : p.ux;
+  p.cyp = cly ? cly * cam.limy64 : p.uy;
+  const double fx = cam.fx64, fy = cam.fy64;
   const double J00 = fx / p.z, J02 = -fx * p.cxp / p.z, J11 = fy / p.z, J12 = -fy * p.cyp / p.z;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    p.T0[k] = J00 * (double)V[k] + J02 * (double)V[8 + k];
-    p.T1[k] = J11 * (double)V[4 + k] + J12 * (double)V[8 + k];
+    p.T0[k] = J00 * V[k] + J02 * V[8 + k];
+    p.T1[k] = J11 * V[4 + k] + J12 * V[8 + k];
   }
   const double St0[3] = {u.S00 * p.T0[0] + u.S01 * p.T0[1] + u.S02 * p.T0[2],
                          u.S01 * p.T0[0] + u.S11 * p.T0[1] + u.S12 * p.T0[2],
@@ -268,8 +268,8 @@ PUV_DEV Proj64 project64(const CamDev& cam, double mx_, double my_, double mz_, 
   p.ha = -0.5 * p.c / p.det;
   p.nb = p.b / p.det;
   p.hc = -0.5 * p.a / p.det;
-  p.mx = fx * p.ux + (double)cam.cx;
-  p.my = fy * p.uy + (double)cam.cy;
+  p.mx = fx * p.ux + cam.cx64;
+  p.my = fy * p.uy + cam.cy64;
   return p;
 }
 

@@ -13,6 +13,8 @@
 // composited set, T_final and n_contrib match the oracle bit for bit.  The composited VALUES are
 // carried in fp64: the image is the fp64 colour rounded once, and the pixel's full
 // colour C = sum c_k a_k T_k + T_final bg is kept for the single-pass backward (K6).
+#include <type_traits>
+
 #include "contract.cuh"
 #include "feed.cuh"
 #include "internal.cuh"
@@ -122,11 +124,14 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
   }
   // examined pairs of a pixel = entries walked until it terminated (inclusive) or the list ended
   uint32_t exam[kFwdPPT], n_comp = 0;
-  // composited-pixel bits for K6: this warp's two words (K6 order: warp (w & 1), row group
-  // k = 2 (w >> 1) + k') of each of the tile's first kMaskCap entries
-  static_assert(kFwdPPT == 2, "the K6 mask layout assumes 2 pixels per K5 thread");
-  uint2* dmask = kMaskCap > 0 ? reinterpret_cast<uint2*>(v.dmask + ((size_t)view * ntiles + tile) * kMaskCap * 8 +
-                                                          (warp & 1) * 4 + 2 * (warp >> 1))
+  // composited-pixel bits for K6 (8 words per entry, K6 order: K6 warp, row group), for each of the
+  // tile's first kMaskCap entries.  PPT 2: this warp's two words (K6 warp (w & 1), row groups
+  // 2 (w >> 1) + k'); PPT 4: the warp IS a K6 warp (8 x 16 pixels), its four words
+  static_assert(kFwdPPT == 2 || kFwdPPT == 4, "the K6 mask layout takes 2 or 4 pixels per K5 thread");
+  using MaskW = std::conditional_t<kFwdPPT == 4, uint4, uint2>;
+  constexpr int kMaskStride = kFwdPPT == 4 ? 2 : 4;   // MaskW units per entry (8 words)
+  MaskW* dmask = kMaskCap > 0 ? reinterpret_cast<MaskW*>(v.dmask + ((size_t)view * ntiles + tile) * kMaskCap * 8 +
+                                                           (kFwdPPT == 4 ? warp * 4 : (warp & 1) * 4 + 2 * (warp >> 1)))
                               : nullptr;
 #pragma unroll
   for (int k = 0; k < kFwdPPT; ++k) exam[k] = 0;
@@ -184,7 +189,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
           const float4 B = sB[j];
           may = block_may_hit(A.x, A.y, A.z, A.w, B.x, B.y, bx0, by0, 7.f, (float)(4 * kFwdPPT - 1));
           const uint32_t e = b0 + j - start;
-          if (!may && kMaskCap > 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(0u, 0u);
+          if (!may && kMaskCap > 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * kMaskStride] = MaskW{};
         }
         mwords[q] = __ballot_sync(0xffffffffu, may);
       }
@@ -207,7 +212,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
       }
       const uint32_t e = b0 + j - start;   // entry index in the tile list
       if (!__any_sync(0xffffffffu, any_of(hit))) {
-        if (kMaskCap > 0 && lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(0u, 0u);
+        if (kMaskCap > 0 && lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * kMaskStride] = MaskW{};
         continue;
       }
       bool comp[kFwdPPT] = {};
@@ -271,11 +276,20 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
       }
 #endif
       if (kMaskCap > 0) {
-        const uint32_t m0 = __ballot_sync(0xffffffffu, comp[0]), m1 = __ballot_sync(0xffffffffu, comp[1]);
+        uint32_t m[kFwdPPT];
+#pragma unroll
+        for (int k = 0; k < kFwdPPT; ++k) m[k] = __ballot_sync(0xffffffffu, comp[k]);
 #if PUV_FWD_POPCNT && !PUV_FWD_BRANCHFREE
-        if (lane == 0) n_comp += __popc(m0) + __popc(m1);   // the warp's composited pairs of this entry
+#pragma unroll
+        for (int k = 0; k < kFwdPPT; ++k)
+          if (lane == 0) n_comp += __popc(m[k]);   // the warp's composited pairs of this entry
 #endif
-        if (lane == 0 && e < (uint32_t)kMaskCap) dmask[(size_t)e * 4] = make_uint2(m0, m1);
+        if (lane == 0 && e < (uint32_t)kMaskCap) {
+          MaskW mw;
+#pragma unroll
+          for (int k = 0; k < kFwdPPT; ++k) reinterpret_cast<uint32_t*>(&mw)[k] = m[k];
+          dmask[(size_t)e * kMaskStride] = mw;
+        }
       }
       if (__all_sync(0xffffffffu, all_of(done))) {
 #if PUV_FWD_CULL

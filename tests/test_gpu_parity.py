@@ -131,6 +131,28 @@ def test_c2_parity_two_views():
     _grad_check(sc, planes, occ, views, dls, grad)
 
 
+@pytest.mark.parametrize("deg", [2, 3])
+def test_sh_degree_parity_small(deg):
+    """SH degrees 2 and 3 on a small two-level atlas (K1 / K7 instantiations with the fp64 SH staging),
+    3 views of a ragged 150x110 image: bit-exact binning and pixel state, images and gradients."""
+    from synth.scenes import _fill_levels, ring
+    rng = np.random.default_rng(np.random.SeedSequence([2602, 23040, 90 + deg]))
+    shapes = [(40, 36), (20, 18)]
+    n = sum(r * c for r, c in shapes)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    pos = d * rng.uniform(0.7, 1.1, size=(n, 1))
+    levels = _fill_levels(rng, pos, deg, shapes, (0, 0, 0))
+    sc = Scene(90 + deg, deg, levels, ring(3, 3.0, 0.4, 150, 110, 140.0), f"SH{deg} small")
+    views = [0, 1, 2]
+    planes, occ, _ = oracle_scene(sc)
+    _, dls = _oracle_dls(sc, planes, occ, views)
+    g, img, loss, grad = _run(sc, views, dls=dls)
+    for vi in views:
+        _parity_view(sc, g, planes, occ, vi, vi, img[vi])
+    _grad_check(sc, planes, occ, views, dls, grad)
+
+
 def test_edge_ragged_multiview_empty_views_bg_mask():
     """Ragged image (100x75, partial tiles), 18 views (> one camera batch), views that see nothing,
     a background colour and a dynamic mask."""

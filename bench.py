@@ -203,8 +203,9 @@ def stage_work(stage, c, D):
         return "alu_fp32", K5_PER_EXAMINED * E + K5_PER_COMPOSITED * P
     if stage == "raster_bwd":       # ~8 per evaluated pair, ~45 per composited pair
         return "alu_fp32", K6_PER_EXAMINED * E + K6_PER_COMPOSITED * P
-    if stage == "project_bwd":      # 9 moments + params read per visible G, texel gradient RMW once per call
-        return "hbm", (72 + 44 + sh) * nv + (D * 4 * 2 * N) / c["views"]
+    if stage == "project_bwd":      # 9 moments per visible (view, G) + every (view, texel) depth key; the texel's
+        # parameters once per call and its gradient written once (train step: overwrite mode)
+        return "hbm", 72 * nv + 4 * N + (44 + sh + 4 * D) * N / c["views"]
     if stage == "loss":
         return "hbm", 12 * 3 * c["HW"]
     return "hbm", 0
@@ -474,9 +475,14 @@ def main():
     roof["other_raster_kernel"] = {k2: rf[other][k2] for k2 in ("kernel", "achieved", "frac", "avg_launch_ms")}
     hbm_stages = {}
     for s_ in ("project", "project_bwd", "loss"):
-        if stage_ms.get(s_, 0) > 0:
-            r = roofline(s_, per_view, D, local_renders, stage_ms[s_],
-                         prof["calls"][s_] / args.steps, peaks, nsm)
+        # the loss runs on the second stream beside the compositing: its event span is not its duration,
+        # so it is rated on the serialised step's time (one launch per view there)
+        ms_, calls_ = stage_ms.get(s_, 0), prof["calls"][s_] / args.steps if s_ in prof["calls"] else 0
+        if s_ == "loss":
+            ms_ = serial.get("loss", 0) * local_renders if serial else 0
+            calls_ = local_renders
+        if ms_ > 0:
+            r = roofline(s_, per_view, D, local_renders, ms_, calls_, peaks, nsm)
             hbm_stages[s_] = {"achieved_gbs": round(r["achieved"], 1), "frac": round(r["frac"], 3)}
 
     cpu = None

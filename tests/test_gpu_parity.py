@@ -153,6 +153,39 @@ def test_sh_degree_parity_small(deg):
     _grad_check(sc, planes, occ, views, dls, grad)
 
 
+@pytest.mark.parametrize("wh", [(1, 1), (17, 3)])
+def test_degenerate_tiny_images_and_empty_atlas(wh):
+    """Degenerate sizes: a 1x1 image (one partial tile, one pixel) and a 17x3 one (two partial
+    tiles), with pixels that terminate (T < 1e-4) and pixels that exhaust their list; then the same
+    scene with every texel unoccupied (nothing visible: zero image, T_final = 1, n_contrib = 0 and
+    an exactly zero gradient)."""
+    W, H = wh
+    rng = np.random.default_rng(7)
+    n = 300
+    mu = rng.uniform(-0.3, 0.3, (n, 3))
+    sh = rng.random((n, 3))
+    logit = rng.normal(0, 1, n)
+    f = 2.0 * max(W, H)
+    cams = [look_at((2.0, 0.2, 0.3), (0, 0, 0), W, H, f), look_at((-1.5, 1.5, 0.5), (0, 0, 0), W, H, f)]
+    for empty in (False, True):
+        sc = tiny_scene(mu, [-2.0] * 3, [1, 0, 0, 0], logit, sh, cams[0], 0)
+        sc.cameras = cams
+        sc.cfg = 97
+        if empty:
+            sc.levels[0].occ[:] = 0
+        planes, occ, _ = oracle_scene(sc)
+        _, dls = _oracle_dls(sc, planes, occ, [0, 1])
+        g, img, loss, grad = _run(sc, [0, 1], dls=dls)
+        for vi in (0, 1):
+            _parity_view(sc, g, planes, occ, vi, vi, img[vi])
+        _grad_check(sc, planes, occ, [0, 1], dls, grad)
+        if empty:
+            assert not img.any() and not grad.any()
+            dbg = puv.debug_tensors(g["layout"], g["cams"], g["R"].state, g["R"].arena, 0)
+            assert dbg["n_visible"] == 0 and dbg["n_keys"] == 0
+            assert (dbg["t_final"].cpu().numpy() == 1.0).all() and not dbg["n_contrib"].cpu().numpy().any()
+
+
 def test_edge_ragged_multiview_empty_views_bg_mask():
     """Ragged image (100x75, partial tiles), 18 views (> one camera batch), views that see nothing,
     a background colour and a dynamic mask."""

@@ -24,6 +24,16 @@ constexpr int kOsWarps = kOsThreads / 32;
 constexpr int kOsItems = PUV_OS_ITEMS;               // per thread
 constexpr int kOsTile = kOsThreads * kOsItems;       // 4096 items per CTA
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagPre = 2u << 30, kCountMask = (1u << 30) - 1u;
+#ifndef PUV_OS_WINDOW
+#define PUV_OS_WINDOW 8
+#endif
+constexpr int kOsWindow = PUV_OS_WINDOW;   // predecessor status words read per look-back round (1 = serial walk)
+#ifndef PUV_OS_STAGE
+#define PUV_OS_STAGE 1
+#endif
+// 1: the scatter goes through shared memory in tile-local digit order, so consecutive threads write
+// consecutive addresses of a digit's run (coalesced) instead of each item straight to its slot
+constexpr bool kOsStage = PUV_OS_STAGE != 0;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -99,10 +109,12 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(const uint32_t* __restri
                                                        uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                        const uint32_t* n_ptr, uint32_t n_fixed, int shift,
                                                        const uint32_t* __restrict__ goff, uint32_t* status,
-                                                       uint32_t* ticket) {
+                                                       uint32_t* ticket, int write_keys) {
   __shared__ uint32_t wh[kOsWarps][256];
   __shared__ uint32_t excl[256];
   __shared__ uint32_t s_tile;
+  __shared__ uint32_t tstart[kOsStage ? 256 : 1], wsum[kOsWarps];
+  __shared__ uint32_t skey[kOsStage ? kOsTile : 1], sval[kOsStage ? kOsTile : 1];
   const uint32_t n = FIRST ? n_fixed : *n_ptr;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   for (int i = threadIdx.x; i < kOsWarps * 256; i += kOsThreads) (&wh[0][0])[i] = 0;
@@ -154,26 +166,73 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(const uint32_t* __restri
       excl[d] = 0;
     } else {
       st_release(st, kFlagAgg | run);
+      // decoupled look-back, kOsWindow predecessors per round (independent loads in flight): sum
+      // aggregates from the nearest tile back until an inclusive prefix; an unpublished tile
+      // restarts the round at that tile (spin)
       uint32_t acc = 0;
       for (int64_t t = (int64_t)tile - 1; t >= 0;) {
-        const uint32_t s = ld_volatile(status + (size_t)t * 256 + d);
-        const uint32_t flag = s & ~kCountMask;
-        if (flag == 0u) continue;             // predecessor not published yet: spin
-        acc += s & kCountMask;
-        if (flag == kFlagPre) break;
-        --t;
+        uint32_t sw[kOsWindow];
+#pragma unroll
+        for (int w = 0; w < kOsWindow; ++w)
+          sw[w] = t - w >= 0 ? ld_volatile(status + (size_t)(t - w) * 256 + d) : kFlagPre;
+        bool found = false;
+        int w = 0;
+        for (; w < kOsWindow; ++w) {
+          const uint32_t flag = sw[w] & ~kCountMask;
+          if (flag == 0u) break;               // not published yet: re-read from tile t - w
+          acc += sw[w] & kCountMask;
+          if (flag == kFlagPre) { found = true; break; }
+        }
+        if (found) break;
+        t -= w;
       }
       st_release(st, kFlagPre | (acc + run));
       excl[d] = acc;
     }
+    if (kOsStage) {
+      // tile-local start of digit d's run: exclusive scan of the tile's digit counts
+      uint32_t x = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      tstart[d] = x - run;   // warp-local exclusive; the warp offsets are added below
+    }
   }
   __syncthreads();
+  if (kOsStage) {
+    uint32_t wo = 0;
+    for (int w = 0; w < warp; ++w) wo += wsum[w];
+    tstart[threadIdx.x] += wo;
+    uint32_t cnt = 0;
+    for (int w = 0; w < kOsWarps; ++w) cnt += wsum[w];
+    __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kOsItems; ++r) {
-    if (dig[r] < 256u) {
-      const uint32_t pos = goff[dig[r]] + excl[dig[r]] + wh[warp][dig[r]] + loc[r];
-      keys_out[pos] = key[r];
-      vals_out[pos] = val[r];
+    for (int r = 0; r < kOsItems; ++r) {
+      if (dig[r] < 256u) {
+        const uint32_t li = tstart[dig[r]] + wh[warp][dig[r]] + loc[r];
+        skey[li] = key[r];
+        sval[li] = val[r];
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += kOsThreads) {
+      const uint32_t k = skey[i];
+      const uint32_t dd = (k >> shift) & 0xffu;
+      const uint32_t pos = goff[dd] + excl[dd] + (i - tstart[dd]);
+      if (write_keys) keys_out[pos] = k;
+      vals_out[pos] = sval[i];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < kOsItems; ++r) {
+      if (dig[r] < 256u) {
+        const uint32_t pos = goff[dig[r]] + excl[dig[r]] + wh[warp][dig[r]] + loc[r];
+        if (write_keys) keys_out[pos] = key[r];
+        vals_out[pos] = val[r];
+      }
     }
   }
 }
@@ -210,11 +269,11 @@ void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cud
   uint32_t* vo[4] = {sv0, sv1, sv0, sorted};
   const int grid = (int)tiles;
   k_os_pass<true><<<grid, kOsThreads, 0, s>>>(ki[0], vi[0], ko[0], vo[0], nullptr, (uint32_t)p.N, 0, ghist, status,
-                                              tickets);
-  for (int pass = 1; pass < 4; ++pass)
+                                              tickets, 1);
+  for (int pass = 1; pass < 4; ++pass)   // the last pass writes only the depth order (its keys are not read)
     k_os_pass<false><<<grid, kOsThreads, 0, s>>>(ki[pass], vi[pass], ko[pass], vo[pass], nvis, 0, 8 * pass,
                                                  ghist + 256 * pass, status + (size_t)pass * 256 * tiles,
-                                                 tickets + pass);
+                                                 tickets + pass, pass < 3 ? 1 : 0);
   count_launches(6);
 }
 

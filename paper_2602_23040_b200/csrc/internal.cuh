@@ -60,6 +60,13 @@ constexpr int kSupT = kSup * kSup;        // tiles per super-tile
 // tile pass, in (depth, gid) order) with the rect test of level 2 applied as they stage a batch,
 // so level 2 (materialising the per-tile lists) runs only for the parity / debug view.
 constexpr bool kDirect = PUV_DIRECT != 0;
+#ifndef PUV_MASK_FILL
+#define PUV_MASK_FILL 1
+#endif
+// K5 writes zero mask words for a warp's entries after it stopped (all its pixels terminated) up to
+// the tile's largest n_contrib, so every word K6 reads is valid and a set bit alone means
+// "composited" (K6 drops its per-pixel e < n_contrib guard)
+constexpr bool kMaskFill = PUV_MASK_FILL != 0 && kDirect && kMaskCap > 0;
 constexpr uint32_t kInvisible = 0xFFFFFFFFu;
 
 // Plane table of a render call; with LPO (PUV_RENDER_LPO) every atlas plane value is read through its

@@ -124,6 +124,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
   }
   // examined pairs of a pixel = entries walked until it terminated (inclusive) or the list ended
   uint32_t exam[kFwdPPT], n_comp = 0;
+  static_assert(!kMaskFill || PUV_FWD_CULL, "the mask fill relies on the filtered walk's stop");
   // composited-pixel bits for K6 (8 words per entry, K6 order: K6 warp, row group), for each of the
   // tile's first kMaskCap entries.  PPT 2: this warp's two words (K6 warp (w & 1), row groups
   // 2 (w >> 1) + k'); PPT 4: the warp IS a K6 warp (8 x 16 pixels), its four words
@@ -302,6 +303,29 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
     ebase += (uint32_t)nb;
     feed.pop(nb);
 #endif
+  }
+  if constexpr (kMaskFill) {
+    // zero words for the entries after this warp stopped, up to the tile's largest n_contrib (the
+    // range K6 walks), so K6 never reads a stale word.  A warp with a live pixel walked (and wrote)
+    // every fed entry; one whose pixels all terminated stopped right after the last termination,
+    // i.e. it wrote entries [0, max exam) (exam = terminating entry + 1; 0 for off-image pixels)
+    const bool wdone = __all_sync(0xffffffffu, all_of(done));
+    uint32_t mx = 0;
+#pragma unroll
+    for (int k = 0; k < kFwdPPT; ++k) mx = max(mx, done[k] ? exam[k] : 0u);
+    const uint32_t wfill = wdone ? __reduce_max_sync(0xffffffffu, mx) : 0xffffffffu;
+    __shared__ uint32_t sLmax[kRasterThreads / 32];
+    uint32_t lm = 0;
+#pragma unroll
+    for (int k = 0; k < kFwdPPT; ++k) lm = max(lm, last[k]);
+    lm = __reduce_max_sync(0xffffffffu, lm);
+    if (lane == 0) sLmax[warp] = lm;
+    __syncthreads();
+    uint32_t Lmax = 0;
+#pragma unroll
+    for (int w = 0; w < kRasterThreads / 32; ++w) Lmax = max(Lmax, sLmax[w]);
+    const uint32_t fe = min(Lmax, (uint32_t)kMaskCap);
+    for (uint32_t e = wfill + lane; e < fe; e += 32) dmask[(size_t)e * kMaskStride] = MaskW{};
   }
 #if PUV_DIRECT
   const uint32_t list_len = ebase;   // the whole list was fed unless every pixel terminated first

@@ -283,7 +283,9 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
         const uint32_t words[4] = {mw.x, mw.y, mw.z, mw.w};
 #pragma unroll
         for (int k = 0; k < kBwdPPT; ++k) {
-          act[k] = e < last[k] && ((words[k] >> lane) & 1u);
+          // kMaskFill: every word up to the tile's largest n_contrib was written by K5 (zero past a
+          // pixel's end), so the bit alone decides; else stale words past a K5 warp's stop need e < last
+          act[k] = (kMaskFill || e < last[k]) && ((words[k] >> lane) & 1u);
           kact[k] = words[k] != 0u;   // a superset of the lanes' act (stale bits past last only add)
           any |= act[k];
         }

@@ -80,7 +80,8 @@ struct StreamSet {
   cudaStream_t s2 = nullptr;     // per-view loss + composite backward of the fused L2 step
   cudaStream_t cp = nullptr;     // host->device uploads of the host-buffer steps
   cudaStream_t cp2 = nullptr;    // device->host downloads of puv_train_step_host_atlas
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t k1 = nullptr;     // K1 of the views after the head (kK1Head), beside their binning
+  cudaEvent_t fork = nullptr, join = nullptr, k1fork = nullptr, k1tail = nullptr;
   std::vector<cudaEvent_t> ev, fev;
   static cudaEvent_t pooled(std::vector<cudaEvent_t>& pool, int v) {
     while ((int)pool.size() <= v) {
@@ -115,6 +116,9 @@ static StreamSet& stream_set(int /*n*/) {
     cudaStreamCreateWithFlags(&ss->s2, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&ss->cp, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&ss->cp2, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ss->k1, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ss->k1fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss->k1tail, cudaEventDisableTiming);
     sets[dev] = ss;
   }
   return *sets[dev];
@@ -514,7 +518,28 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
   const Plan& p = c.plan;
   cudaMemsetAsync(c.views.hdr, 0, sizeof(ViewHdr) * n_views, s);
   launch_begin_call(p, c.views, arena_bytes / 4, s);
-  for (int v0 = 0; v0 < n_views; v0 += kCamBatch) {
+  StreamSet& ss = stream_set(p.nscratch);
+  std::lock_guard<std::mutex> lock(ss.mu);
+  // K1 head split: project the first kK1Head views first (one more pass over the atlas) so their
+  // binning starts while K1 of the other views runs on its own stream; those views' binning waits
+  // for that K1 (k1tail).  Device-resident atlas only (the texel-chunk host path keeps one K1).
+  const bool head_split = kK1Head > 0 && !tin && n_views > kK1Head && n_views <= kCamBatch;
+  if (head_split) {
+    cudaEventRecord(ss.k1fork, s);
+    CamBatch ch;
+    ch.v0 = 0;
+    ch.n = kK1Head;
+    for (int i = 0; i < ch.n; ++i) ch.c[i] = cam_dev(cams[i]);
+    { StageScope sc(PUV_STAGE_PROJECT, s); launch_project(p, c.views, c.P, atlas_occ, ch, s); }
+    cudaStreamWaitEvent(ss.k1, ss.k1fork, 0);
+    CamBatch ct;
+    ct.v0 = kK1Head;
+    ct.n = n_views - kK1Head;
+    for (int i = 0; i < ct.n; ++i) ct.c[i] = cam_dev(cams[kK1Head + i]);
+    { StageScope sc(PUV_STAGE_PROJECT, ss.k1); launch_project(p, c.views, c.P, atlas_occ, ct, ss.k1); }
+    cudaEventRecord(ss.k1tail, ss.k1);
+  }
+  for (int v0 = 0; v0 < n_views && !head_split; v0 += kCamBatch) {
     CamBatch cb;
     cb.v0 = v0;
     cb.n = n_views - v0 < kCamBatch ? n_views - v0 : kCamBatch;
@@ -531,8 +556,6 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
   }
   // Pipeline: view v is depth-sorted and binned on binning stream v % nscratch (its own scratch
   // block) while earlier views composite on `s`; `s` waits on view v's binning event only.
-  StreamSet& ss = stream_set(p.nscratch);
-  std::lock_guard<std::mutex> lock(ss.mu);
   cudaEventRecord(ss.fork, s);
   for (int i = 0; i < p.nscratch; ++i) cudaStreamWaitEvent(ss.s[i], ss.fork, 0);
   if (hook) {
@@ -547,6 +570,7 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
   for (int v = 0; v < n_views; ++v) {
     const int i = v % p.nscratch;
     cudaStream_t bs = serial ? s : ss.s[i];
+    if (head_split && v >= kK1Head) cudaStreamWaitEvent(bs, ss.k1tail, 0);
     void* scratch = (char*)state + p.scratch0 + (size_t)i * p.scratch_stride;
     { StageScope sc(PUV_STAGE_DEPTH_SORT, bs); launch_depth_sort(p, c.views, scratch, v, bs); }
     { StageScope sc(PUV_STAGE_BIN, bs); launch_bin(p, c.views, scratch, (uint32_t*)arena, v, bs, !kDirect); }

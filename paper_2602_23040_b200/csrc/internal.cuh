@@ -14,6 +14,11 @@
 #endif
 constexpr bool kLno = PUV_LNO != 0;
 
+#ifndef PUV_K1_HEAD
+#define PUV_K1_HEAD 0
+#endif
+constexpr int kK1Head = PUV_K1_HEAD;   // views projected ahead of the rest (0: one K1 for all views)
+
 #ifndef PUV_STEP_OVERLAP
 #define PUV_STEP_OVERLAP 0
 #endif

@@ -313,7 +313,7 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
     uint32_t mx = 0;
 #pragma unroll
     for (int k = 0; k < kFwdPPT; ++k) mx = max(mx, done[k] ? exam[k] : 0u);
-    const uint32_t wfill = wdone ? __reduce_max_sync(0xffffffffu, mx) : 0xffffffffu;
+    const uint32_t wfill = __reduce_max_sync(0xffffffffu, mx);   // used only when wdone
     __shared__ uint32_t sLmax[kRasterThreads / 32];
     uint32_t lm = 0;
 #pragma unroll
@@ -325,7 +325,8 @@ __global__ void PUV_FWD_BOUNDS k_raster_fwd(const uint32_t* __restrict__ arena, 
 #pragma unroll
     for (int w = 0; w < kRasterThreads / 32; ++w) Lmax = max(Lmax, sLmax[w]);
     const uint32_t fe = min(Lmax, (uint32_t)kMaskCap);
-    for (uint32_t e = wfill + lane; e < fe; e += 32) dmask[(size_t)e * kMaskStride] = MaskW{};
+    if (wdone)
+      for (uint32_t e = wfill + lane; e < fe; e += 32) dmask[(size_t)e * kMaskStride] = MaskW{};
   }
 #if PUV_DIRECT
   const uint32_t list_len = ebase;   // the whole list was fed unless every pixel terminated first

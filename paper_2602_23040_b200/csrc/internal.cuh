@@ -66,7 +66,7 @@ constexpr int kSupT = kSup * kSup;        // tiles per super-tile
 // so level 2 (materialising the per-tile lists) runs only for the parity / debug view.
 constexpr bool kDirect = PUV_DIRECT != 0;
 #ifndef PUV_MASK_FILL
-#define PUV_MASK_FILL 1
+#define PUV_MASK_FILL 0
 #endif
 // K5 writes zero mask words for a warp's entries after it stopped (all its pixels terminated) up to
 // the tile's largest n_contrib, so every word K6 reads is valid and a set bit alone means

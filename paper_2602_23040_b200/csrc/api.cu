@@ -573,6 +573,9 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
     if (head_split && v >= kK1Head) cudaStreamWaitEvent(bs, ss.k1tail, 0);
     void* scratch = (char*)state + p.scratch0 + (size_t)i * p.scratch_stride;
     { StageScope sc(PUV_STAGE_DEPTH_SORT, bs); launch_depth_sort(p, c.views, scratch, v, bs); }
+#ifdef PUV_SORT_TWICE   // measurement only: the marginal step cost of the depth sort's SM time
+    launch_depth_sort(p, c.views, scratch, v, bs);
+#endif
     { StageScope sc(PUV_STAGE_BIN, bs); launch_bin(p, c.views, scratch, (uint32_t*)arena, v, bs, !kDirect); }
     cudaEvent_t done = ss.view_event(v);
     cudaEventRecord(done, bs);

@@ -57,12 +57,6 @@ constexpr int kRedRow = 34;   // row stride (doubles) of the transpose buffer: 4
 #ifndef PUV_BWD_BATCH
 #define PUV_BWD_BATCH 64
 #endif
-#ifndef PUV_BWD_PIPE
-#define PUV_BWD_PIPE 0
-#endif
-// 1: software-pipelined moment reduction -- the warp reduction and atomics of entry j-1 are issued
-// in the same basic block as the pixel bodies of entry j, so the shuffle-level latency chain
-// interleaves with independent fp64 work instead of ending every iteration
 #ifndef PUV_BWD_KSKIP
 #define PUV_BWD_KSKIP 0
 #endif
@@ -209,18 +203,6 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
 #pragma unroll
   for (int w = 0; w < kBwdThreads / 32; ++w) bmax = max(bmax, smax[w]);
 
-  // the moment reduction of one entry (9 values over the warp, then 9 fp64 atomics into its slot)
-  auto commit = [&](double (&x)[9], uint32_t gid, bool on) {
-    const double s = warp_reduce9_shfl(x);
-    double* dst = g2 + 9 * (size_t)gid;
-    if (on && (lane & 3) == 0) atomicAdd(dst + (lane >> 2), s);
-    if (on && lane == 1) atomicAdd(dst + 8, x[8]);
-  };
-#if PUV_BWD_PIPE
-  double pg[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // the previous walked entry's per-lane moments
-  uint32_t pgid = 0;
-  bool pend = false;
-#endif
 #if PUV_DIRECT
   for (uint32_t lo = 0; lo < bmax;) {
     const int nb = feed.next(list1, sorted_v, rect_v, tx, ty);
@@ -342,9 +324,6 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       // rare: o >= 0.99) capped variant, so the common path carries no cap logic at all.
       auto bodies = [&](auto cap_tag) {
         constexpr bool kCap = decltype(cap_tag)::value;
-#if PUV_BWD_PIPE
-        commit(pg, pgid, pend);   // entry j-1's reduction, interleavable with the bodies below
-#endif
 #pragma unroll
         for (int k = 0; k < kBwdPPT; ++k) {
 #if PUV_BWD_KSKIP
@@ -393,14 +372,10 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
       gv[3] = dx * sdy;
       // raw moments into the (view, Gaussian) slot; K7 turns them into dL/d(mx, my, ha, nb, hc)
 #ifndef PUV_BWD_SMEM_RED
-#if PUV_BWD_PIPE
-#pragma unroll
-      for (int q = 0; q < 9; ++q) pg[q] = gv[q];
-      pgid = sG[j];
-      pend = true;
-#else
-      commit(gv, sG[j], true);
-#endif
+      const double s = warp_reduce9_shfl(gv);
+      double* dst = g2 + 9 * (size_t)sG[j];
+      if ((lane & 3) == 0) atomicAdd(dst + (lane >> 2), s);
+      if (lane == 1) atomicAdd(dst + 8, gv[8]);
 #else
       const double s = warp_sum9(gv, sRed[warp], lane);
       if (lane < 27 && lane % 3 == 0) atomicAdd(g2 + 9 * (size_t)sG[j] + lane / 3, s);
@@ -411,9 +386,6 @@ __global__ void PUV_BWD_BOUNDS k_raster_bwd(const uint32_t* __restrict__ arena, 
     feed.pop(nb);
 #endif
   }
-#if PUV_BWD_PIPE
-  if (pend) commit(pg, pgid, true);   // the last walked entry
-#endif
 }
 
 void launch_raster_bwd(const Plan& p, const Views& v, const uint32_t* arena, const float* dL_dimages, int view0,

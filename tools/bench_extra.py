@@ -24,7 +24,7 @@ from paper_2602_23040_b200 import puv  # noqa: E402
 from synth.scenes import make_scene, motion_masks, moving_region_masks, ring, rho_scene  # noqa: E402
 
 
-def bench_label(steps=5, warmup=2, region=True):
+def bench_label(steps=5, warmup=2, region=True, radius=None):
     """region=True: the motion masks of a spatially coherent moving part (a 0.6 m ball around the
     scene point nearest to the densest texel neighbourhood, synth.moving_region_masks); False: the
     round-1 seeded disc masks (unstructured: their OR over 55 cameras labels ~97 % dynamic)."""
@@ -41,7 +41,8 @@ def bench_label(steps=5, warmup=2, region=True):
         cand = mu[rng.choice(mu.shape[0], 64, replace=False)]
         # the candidate with the most texels within 0.6 m: a moving part inside one of the blobs
         counts = [(np.linalg.norm(mu[::16] - c, axis=1) <= 0.6).sum() for c in cand]
-        centre, radius = cand[int(np.argmax(counts))], 0.6
+        centre = cand[int(np.argmax(counts))]
+        radius = LABEL_RADIUS if radius is None else radius
         masks_np = moving_region_masks(sc, list(range(len(sc.cameras))), centre, radius)
         inside = float((np.linalg.norm(mu - centre, axis=1) <= radius).mean())
     else:
@@ -69,8 +70,19 @@ def bench_label(steps=5, warmup=2, region=True):
             "gpu_launches_per_call": (puv.kernel_launches() - l0) // steps,
             "moving_ball_fraction": inside if region else None,
             "workload": "C4 atlas 1024^2 SH3, 55 dome cameras 1920x1080, " +
-                        ("masks of a moving 0.6 m ball (synth.moving_region_masks)" if region else
+                        (f"masks of a moving {radius} m ball (synth.moving_region_masks)" if region else
                          "seeded disc motion masks")}
+
+
+# radius of the moving ball of the NEXT-3 row: chosen with label_sweep so that Alg. 1 labels about
+# the 25 % dynamic texels of BJ.configs[3] (the OR over 55 dome cameras labels every Gaussian on a
+# ray through the ball in any view, so the labelled fraction grows much faster than the ball)
+LABEL_RADIUS = 0.6
+
+
+def bench_label_sweep():
+    """Labelled (dynamic) fraction and throughput of Alg. 1 against the moving-ball radius."""
+    return [bench_label(steps=2, warmup=1, radius=r) for r in (0.05, 0.1, 0.15, 0.2, 0.3, 0.45, 0.6)]
 
 
 def _time_steps(R, planes, occ, targets, steps, warmup):
@@ -255,6 +267,6 @@ def bench_lpo(steps=5, warmup=3):
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["label", "rho", "objective", "lpo"]
-    rows = {"label": bench_label, "rho": bench_rho, "objective": bench_objective, "lpo": bench_lpo}
+    rows = {"label": bench_label, "label_sweep": bench_label_sweep, "rho": bench_rho, "objective": bench_objective, "lpo": bench_lpo}
     for w in which:
         print(json.dumps(rows[w]()), flush=True)

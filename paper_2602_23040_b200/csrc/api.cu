@@ -504,7 +504,10 @@ struct L2Hook {
 // Host-link overlap of puv_train_step_host_atlas: the atlas arrives in texel chunks and K1 projects
 // each chunk once it has landed (`ready`); the gradient leaves in texel chunks, each copied out
 // as soon as K7 has finished it (`done`).
-constexpr int kTexelChunks = 4;
+#ifndef PUV_TEXEL_CHUNKS
+#define PUV_TEXEL_CHUNKS 4
+#endif
+constexpr int kTexelChunks = PUV_TEXEL_CHUNKS;
 struct TexelPipe {
   int n;                              // chunks (<= kTexelChunks)
   int bound[kTexelChunks + 1];        // texel ranges [bound[i], bound[i+1])

@@ -82,7 +82,7 @@ struct StreamSet {
   cudaStream_t cp2 = nullptr;    // device->host downloads of puv_train_step_host_atlas
   cudaStream_t k1 = nullptr;     // K1 of the views after the head (kK1Head), beside their binning
   cudaEvent_t fork = nullptr, join = nullptr, k1fork = nullptr, k1tail = nullptr;
-  std::vector<cudaEvent_t> ev, fev;
+  std::vector<cudaEvent_t> ev, fev, sev;
   static cudaEvent_t pooled(std::vector<cudaEvent_t>& pool, int v) {
     while ((int)pool.size() <= v) {
       cudaEvent_t e;
@@ -93,6 +93,7 @@ struct StreamSet {
   }
   cudaEvent_t view_event(int v) { return pooled(ev, v); }
   cudaEvent_t fwd_event(int v) { return pooled(fev, v); }
+  cudaEvent_t sort_event(int g) { return pooled(sev, g); }
 };
 
 static StreamSet& stream_set(int /*n*/) {
@@ -251,11 +252,11 @@ Plan make_plan(const puv_layout& L, int n_views, int W, int H) {
   // binning scratch: one block per binning stream; offsets below are relative to a block
   size_t soff = 0;
   auto stake = [&](size_t bytes) { const size_t o = soff; soff += align_up(bytes); return o; };
-  p.sk0 = stake(4 * N);
-  p.sv0 = stake(4 * N);
-  p.sk1 = stake(4 * N);
-  p.sv1 = stake(4 * N);
-  p.hist = stake(depth_sort_scratch_bytes(N));
+  p.sk0 = stake(4 * N * kSortGroup);   // onesweep ping-pong of a sort group of views
+  p.sv0 = stake(4 * N * kSortGroup);
+  p.sk1 = stake(4 * N * kSortGroup);
+  p.sv1 = stake(4 * N * kSortGroup);
+  p.hist = stake(depth_sort_scratch_bytes(N) * kSortGroup);
   p.koff = stake(4 * (N + 1));
   p.bsum = stake(4 * (N / 2048 + 2));
   p.cnt = stake(4 * (size_t)kNbMax * p.ntiles);
@@ -575,10 +576,26 @@ static void render_pipeline(const Common& c, const uint8_t* atlas_occ, int n_vie
     cudaStream_t bs = serial ? s : ss.s[i];
     if (head_split && v >= kK1Head) cudaStreamWaitEvent(bs, ss.k1tail, 0);
     void* scratch = (char*)state + p.scratch0 + (size_t)i * p.scratch_stride;
-    { StageScope sc(PUV_STAGE_DEPTH_SORT, bs); launch_depth_sort(p, c.views, scratch, v, bs); }
+    if (kSortGroup == 1) {
+      { StageScope sc(PUV_STAGE_DEPTH_SORT, bs); launch_depth_sort(p, c.views, scratch, v, 1, bs); }
 #ifdef PUV_SORT_TWICE   // measurement only: the marginal step cost of the depth sort's SM time
-    launch_depth_sort(p, c.views, scratch, v, bs);
+      launch_depth_sort(p, c.views, scratch, v, 1, bs);
 #endif
+    } else {
+      // sort group gi = views [gi G, gi G + G) depth-sorted together on binning stream gi % nscratch
+      // (its scratch block holds G views of onesweep scratch); each view's tile pass then runs on
+      // stream v % nscratch as before, after its group's sort
+      const int gi = v / kSortGroup;
+      if (v % kSortGroup == 0) {
+        const int si = gi % p.nscratch;
+        cudaStream_t gs = serial ? s : ss.s[si];
+        void* gscratch = (char*)state + p.scratch0 + (size_t)si * p.scratch_stride;
+        const int nv = n_views - v < kSortGroup ? n_views - v : kSortGroup;
+        { StageScope sc(PUV_STAGE_DEPTH_SORT, gs); launch_depth_sort(p, c.views, gscratch, v, nv, gs); }
+        cudaEventRecord(ss.sort_event(gi), gs);
+      }
+      if (!serial) cudaStreamWaitEvent(bs, ss.sort_event(gi), 0);
+    }
     { StageScope sc(PUV_STAGE_BIN, bs); launch_bin(p, c.views, scratch, (uint32_t*)arena, v, bs, !kDirect); }
     cudaEvent_t done = ss.view_event(v);
     cudaEventRecord(done, bs);

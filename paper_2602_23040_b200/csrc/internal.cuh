@@ -38,6 +38,11 @@ constexpr int kNbMax = 1024;              // max key blocks of the stable tile p
 #define PUV_BIN_STREAMS 4
 #endif
 constexpr int kBinStreams = PUV_BIN_STREAMS;  // views binned concurrently (one scratch block each)
+#ifndef PUV_SORT_GROUP
+#define PUV_SORT_GROUP 1
+#endif
+// views depth-sorted by one set of onesweep launches (grid.y); their tile passes stay per view
+constexpr int kSortGroup = PUV_SORT_GROUP;
 #ifndef PUV_BIN_PRIORITY
 #define PUV_BIN_PRIORITY 0
 #endif
@@ -189,7 +194,7 @@ size_t bin_scratch_bytes(size_t N, int ntiles);
 // ---- launchers (all asynchronous on `s`) ----
 void launch_project(const Plan& p, const Views& v, const PlaneTab& P, const uint8_t* occ, const CamBatch& cb,
                     cudaStream_t s, int g0 = 0, int g1 = -1);
-void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cudaStream_t s);
+void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, int nv, cudaStream_t s);
 void launch_bin(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s, bool level2);
 void launch_bin_level2(const Plan& p, const Views& v, void* state, uint32_t* arena, int view, cudaStream_t s);
 void launch_raster_fwd(const Plan& p, const Views& v, const uint32_t* arena, float* images, int view0, int n_views,

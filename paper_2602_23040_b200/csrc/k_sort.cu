@@ -52,7 +52,10 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 }
 
 __global__ void __launch_bounds__(kOsThreads) k_os_hist(const uint32_t* __restrict__ keys, uint32_t n,
-                                                       uint32_t* __restrict__ ghist) {
+                                                       uint32_t* __restrict__ ghist, size_t vstride) {
+  // grid.y: the views of a sort group (keys of view y at keys + y n, its scratch at + y vstride)
+  keys += (size_t)blockIdx.y * n;
+  ghist += (size_t)blockIdx.y * vstride;
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += kOsThreads) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -84,7 +87,12 @@ __global__ void __launch_bounds__(kOsThreads) k_os_hist(const uint32_t* __restri
 }
 
 // ghist[4][256] counts -> exclusive offsets in place; n_vis; reset the pass tickets.
-__global__ void __launch_bounds__(256) k_os_scan(uint32_t* ghist, uint32_t* tickets, uint32_t* n_vis) {
+__global__ void __launch_bounds__(256) k_os_scan(uint32_t* ghist, uint32_t* tickets, uint32_t* n_vis,
+                                                 size_t vstride, size_t nvstride) {
+  // block x: view x of the sort group
+  ghist += (size_t)blockIdx.x * vstride;
+  tickets += (size_t)blockIdx.x * vstride;
+  n_vis += (size_t)blockIdx.x * nvstride;
   __shared__ uint32_t s[256];
   for (int p = 0; p < 4; ++p) {
     const uint32_t c = ghist[p * 256 + threadIdx.x];
@@ -109,12 +117,25 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(const uint32_t* __restri
                                                        uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                        const uint32_t* n_ptr, uint32_t n_fixed, int shift,
                                                        const uint32_t* __restrict__ goff, uint32_t* status,
-                                                       uint32_t* ticket, int write_keys) {
+                                                       uint32_t* ticket, int write_keys, uint32_t kvstride,
+                                                       size_t vstride, size_t nvstride) {
   __shared__ uint32_t wh[kOsWarps][256];
   __shared__ uint32_t excl[256];
   __shared__ uint32_t s_tile;
   __shared__ uint32_t tstart[kOsStage ? 256 : 1], wsum[kOsWarps];
   __shared__ uint32_t skey[kOsStage ? kOsTile : 1], sval[kOsStage ? kOsTile : 1];
+  {  // grid.y: view y of the sort group -- its keys / values (stride kvstride), its histogram
+     // offsets, look-back status words and ticket (stride vstride), its visible count (nvstride)
+    const size_t y = blockIdx.y;
+    keys_in += y * kvstride;
+    if (!FIRST) vals_in += y * kvstride;
+    keys_out += y * kvstride;
+    vals_out += y * kvstride;
+    goff += y * vstride;
+    status += y * vstride;
+    ticket += y * vstride;
+    if (!FIRST) n_ptr += y * nvstride;
+  }
   const uint32_t n = FIRST ? n_fixed : *n_ptr;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   for (int i = threadIdx.x; i < kOsWarps * 256; i += kOsThreads) (&wh[0][0])[i] = 0;
@@ -242,38 +263,47 @@ size_t depth_sort_scratch_bytes(size_t N) {
   return 4 * (4 * 256 * tiles + 4 * 256 + 8);
 }
 
-void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, cudaStream_t s) {
+void launch_depth_sort(const Plan& p, const Views& v, void* state, int view, int nv, cudaStream_t s) {
+  // views [view, view + nv) in one set of launches (grid.y = view of the group, nv <= kSortGroup):
+  // the per-view sorts are independent (own histograms, tickets, look-back chains), batched only
+  // for parallelism -- one view's ~836k visible keys fill ~1.4 onesweep CTAs per SM
   char* st = (char*)state;
-  uint32_t* sk0 = (uint32_t*)(st + p.sk0);
+  const size_t N = p.N;
+  uint32_t* sk0 = (uint32_t*)(st + p.sk0);   // [kSortGroup][N] each
   uint32_t* sv0 = (uint32_t*)(st + p.sv0);
   uint32_t* sk1 = (uint32_t*)(st + p.sk1);
   uint32_t* sv1 = (uint32_t*)(st + p.sv1);
-  const size_t tiles = ((size_t)p.N + kOsTile - 1) / kOsTile;
-  uint32_t* status = (uint32_t*)(st + p.hist);              // [4][tiles][256]
-  uint32_t* ghist = status + 4 * 256 * tiles;               // [4][256]
-  uint32_t* tickets = ghist + 4 * 256;                      // [4]
-  const uint32_t* depth = v.depth + (size_t)view * p.N;
+  const size_t tiles = (N + kOsTile - 1) / kOsTile;
+  // per view: status [4][tiles][256], ghist [4][256], tickets [4] (+ pad): depth_sort_scratch_bytes
+  const size_t vstride = depth_sort_scratch_bytes(N) / 4;
+  uint32_t* status = (uint32_t*)(st + p.hist);
+  uint32_t* ghist = status + 4 * 256 * tiles;
+  uint32_t* tickets = ghist + 4 * 256;
+  const uint32_t* depth = v.depth + (size_t)view * N;
   uint32_t* nvis = &v.hdr[view].n_vis;
-  uint32_t* sorted = v.sorted + (size_t)view * p.N;
-  cudaMemsetAsync(status, 0, 4 * (4 * 256 * tiles + 4 * 256), s);
+  const size_t nvstride = sizeof(ViewHdr) / sizeof(uint32_t);
+  static_assert(sizeof(ViewHdr) % sizeof(uint32_t) == 0, "ViewHdr stride in words");
+  uint32_t* sorted = v.sorted + (size_t)view * N;
+  cudaMemsetAsync(status, 0, 4 * vstride * nv, s);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t hwant = ((size_t)p.N + 4 * kOsThreads - 1) / (4 * kOsThreads);
-  const int hb = (int)(hwant < (size_t)4 * nsm ? (hwant > 0 ? hwant : 1) : (size_t)4 * nsm);
-  k_os_hist<<<hb, kOsThreads, 0, s>>>(depth, (uint32_t)p.N, ghist);
-  k_os_scan<<<1, 256, 0, s>>>(ghist, tickets, nvis);
+  const size_t hwant = (N + 4 * kOsThreads - 1) / (4 * kOsThreads);
+  const size_t hcap = (size_t)4 * nsm / nv > 0 ? (size_t)4 * nsm / nv : 1;
+  const int hb = (int)(hwant < hcap ? (hwant > 0 ? hwant : 1) : hcap);
+  k_os_hist<<<dim3(hb, nv), kOsThreads, 0, s>>>(depth, (uint32_t)N, ghist, vstride);
+  k_os_scan<<<nv, 256, 0, s>>>(ghist, tickets, nvis, vstride, nvstride);
   const uint32_t* ki[4] = {depth, sk0, sk1, sk0};
   const uint32_t* vi[4] = {nullptr, sv0, sv1, sv0};
   uint32_t* ko[4] = {sk0, sk1, sk0, sk1};
   uint32_t* vo[4] = {sv0, sv1, sv0, sorted};
-  const int grid = (int)tiles;
-  k_os_pass<true><<<grid, kOsThreads, 0, s>>>(ki[0], vi[0], ko[0], vo[0], nullptr, (uint32_t)p.N, 0, ghist, status,
-                                              tickets, 1);
+  const dim3 grid((unsigned)tiles, nv);
+  k_os_pass<true><<<grid, kOsThreads, 0, s>>>(ki[0], vi[0], ko[0], vo[0], nullptr, (uint32_t)N, 0, ghist, status,
+                                              tickets, 1, (uint32_t)N, vstride, nvstride);
   for (int pass = 1; pass < 4; ++pass)   // the last pass writes only the depth order (its keys are not read)
     k_os_pass<false><<<grid, kOsThreads, 0, s>>>(ki[pass], vi[pass], ko[pass], vo[pass], nvis, 0, 8 * pass,
                                                  ghist + 256 * pass, status + (size_t)pass * 256 * tiles,
-                                                 tickets + pass, pass < 3 ? 1 : 0);
+                                                 tickets + pass, pass < 3 ? 1 : 0, (uint32_t)N, vstride, nvstride);
   count_launches(6);
 }
 

@@ -16,7 +16,7 @@ template <int DEG, bool LPO>
 #define PUV_PROJ_SH_SMEM 1
 #endif
 #ifndef PUV_PROJ_MINB
-#define PUV_PROJ_MINB 3
+#define PUV_PROJ_MINB 4
 #endif
 __global__ void __launch_bounds__(128, PUV_PROJ_MINB) k_project(PlaneTab P, PosMode pm, const uint8_t* __restrict__ occ, int N,
                                                  const __grid_constant__ CamBatch cb, Views v, int gx, int gy,

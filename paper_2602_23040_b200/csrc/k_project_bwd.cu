@@ -29,6 +29,12 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+#ifndef PUV_PBWD_STAGES
+#define PUV_PBWD_STAGES 4
+#endif
+constexpr int kPbwdStages = PUV_PBWD_STAGES;   // staging buffers: views in flight = stages - 1
 
 #ifndef PUV_PBWD_SH_SMEM
 #define PUV_PBWD_SH_SMEM 1
@@ -88,8 +94,8 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
 
 #if PUV_PBWD_PREFETCH
   // double-buffered per-thread staging of (depth key, 9 moments) of view i + 1 while view i runs
-  __shared__ double sG2[2][9][128];
-  __shared__ uint32_t sDep[2][128];
+  __shared__ double sG2[kPbwdStages][9][128];
+  __shared__ uint32_t sDep[kPbwdStages][128];
   const int tid = threadIdx.x;
   auto prefetch = [&](int i, int buf) {
     if (i < cb.n) {
@@ -101,14 +107,15 @@ __global__ void __launch_bounds__(128, PUV_PBWD_MINB) k_project_bwd(PlaneTab P, 
     }
     cp_async_commit();
   };
-  prefetch(0, 0);
+#pragma unroll
+  for (int j = 0; j < kPbwdStages - 1; ++j) prefetch(j, j);
 #endif
   for (int i = 0; i < cb.n; ++i) {
     const size_t o = (size_t)(cb.v0 + i) * N + g;
 #if PUV_PBWD_PREFETCH
-    prefetch(i + 1, (i + 1) & 1);
-    cp_async_wait1();   // view i's group has landed (only view i + 1's may be pending)
-    const int buf = i & 1;
+    prefetch(i + kPbwdStages - 1, (i + kPbwdStages - 1) % kPbwdStages);
+    cp_async_wait<kPbwdStages - 1>();   // view i's group has landed (only the next views' may be pending)
+    const int buf = i % kPbwdStages;
     if (sDep[buf][tid] == kInvisible) continue;
     // K6's raw moments (Mx, My, Mxx, Mxy, Myy, dL/do, dL/drgb): see k_raster_bwd.cu
     const double Mx = sG2[buf][0][tid], My = sG2[buf][1][tid], Mxx = sG2[buf][2][tid], Mxy = sG2[buf][3][tid],

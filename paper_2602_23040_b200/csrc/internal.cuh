@@ -58,9 +58,9 @@ constexpr int kBinPriority = PUV_BIN_PRIORITY;  // 1: binning streams at the hig
 // fp32 skip test (entries beyond the cap: replay).  DESIGN.md §6.
 constexpr int kMaskCap = PUV_DMASK ? PUV_DMASK_CAP : 0;
 #ifndef PUV_FWD_GROUP
-#define PUV_FWD_GROUP 1
+#define PUV_FWD_GROUP 4
 #endif
-constexpr int kFwdGroup = PUV_FWD_GROUP;  // consecutive views per forward-composite launch
+constexpr int kFwdGroup = PUV_FWD_GROUP;  // consecutive views per forward-composite launch (4: K5 47.3 -> 42.8 ms/step)
 constexpr int kSup = 4;                   // tiles per super-tile side (level 1 of the tile pass)
 constexpr int kSupT = kSup * kSup;        // tiles per super-tile
 #ifndef PUV_DIRECT
